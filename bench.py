@@ -1,0 +1,376 @@
+"""Benchmark: evaluated neighbours/s (NSE/s) of the SAW search at L=201.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+One "step" = one batch of walks (BASELINE config 4): every GPU runs
+`--walkers-per-gpu` (default 2^20) independent walks of n = 8*D steps at
+L=201 with seeds derived on device from (master_seed=1, batch, global walker),
+then the batch is merged across ranks (NCCL all-reduce MIN/SUM, 16-88 B).
+Weak scaling: per-GPU work is fixed as N grows.
+
+value  = sum over ranks of steps*(D-1) / max over ranks of the device time of
+         the K timed batches (CUDA events on the launching stream, L2 flushed
+         between batches).
+e2e    = the same metric through the reference-facing host-buffer drop-in
+         (sk_saw_batch_host == _kernels.saw_batch): host seeds in, per-walk
+         outputs out, copies inside the timed region.
+--impl reference: the reference's CPU algorithm (the oracle port,
+         oracle/sokol_oracle.c, all host cores) on a bounded sample of the
+         same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L_DEFAULT = 201
+METRIC = "evaluated neighbours/sec (NSE/s) at L=201"
+UNIT = "NSE/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--length", type=int, default=L_DEFAULT)
+    ap.add_argument("--walkers-per-gpu", type=int, default=1 << 20)
+    ap.add_argument("--walk-factor", type=int, default=8)
+    ap.add_argument("--master-seed", type=int, default=1)
+    ap.add_argument("--variant", default="auto", choices=["auto", "scalar", "fast"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-walkers", type=int, default=0, help="walkers per e2e step (0 = walkers-per-gpu)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_baseline(L: int, walk_factor: int, master: int, seconds: float) -> dict:
+    """The reference algorithm on all host cores (oracle port), bounded."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    oracle.build()
+    cores = oracle.num_procs()
+    d = (L + 1) // 2
+    n = walk_factor * d
+    per = 4 * cores  # walkers = 4 * os.cpu_count()
+    oracle.batch_outputs(L, n, oracle.derive_walk_seeds(master, 10**6, cores))  # warm-up
+    total = 0
+    walks = 0
+    t0 = time.perf_counter()
+    b = 0
+    while True:
+        seeds = oracle.derive_walk_seeds(master, b, per)
+        _, _, st, _ = oracle.batch_outputs(L, n, seeds)
+        total += int(st.sum()) * (d - 1)
+        walks += per
+        b += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": total / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{walks} walks of L={L}, n={n} ({b} batches of {per}, master_seed={master}) in {el:.1f}s "
+                      f"on {cores} threads (oracle/sokol_oracle.c, pthreads)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    L = args.length
+    d = (L + 1) // 2
+    # each step is a bounded sample (~seconds) of the same workload
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(L, args.walk_factor, args.master_seed, 1.0)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(L, args.walk_factor, args.master_seed, max(2.0, args.cpu_seconds / max(1, args.steps))))
+    v = sum(x["value"] for x in vals) / len(vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    per_step_nse = 4 * cb["cores"] * 8 * d * (d - 1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_nse / v * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic: random starts from derive_walk_seed(1, batch, walker)",
+        "config": {"workload": f"L={L} throughput (bounded CPU sample per step)", "L": L, "n": args.walk_factor * d,
+                   "walkers_per_step": 4 * cb["cores"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ native --
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_15962_b200 import _lib, engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    lib = _lib.load()
+    _lib.set_variant({"auto": 0, "scalar": 1, "fast": 2}[args.variant])
+
+    L = args.length
+    D = (L + 1) // 2
+    nw = (D + 63) // 64
+    n = args.walk_factor * D
+    Wg = args.walkers_per_gpu
+    begin = rank * Wg
+    stream = torch.cuda.current_stream(dev)
+    summ = torch.empty(engine.SUMMARY_WORDS, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def launch(batch):
+        _lib.check(lib.sk_saw_batch(L, n, None, args.master_seed, batch, begin, Wg, None, None, None, None,
+                                    summ.data_ptr(), stream.cuda_stream))
+
+    def merge():
+        loc = engine.decode_summary(summ.cpu().numpy().view(np.uint64), nw)
+        if pg is None:
+            return loc
+        return engine.merge_across_ranks(loc, loc.steps_sum if loc else 0, nw, pg, dev)
+
+    for b in range(args.warmup):
+        launch(1000 + b)
+        merge()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    total_steps = 0
+    best = None
+    if pg is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for b in range(args.steps):
+        flush.zero_()
+        starts[b].record(stream)
+        launch(b)
+        res = merge()  # 80-byte D2H (+ NCCL MIN/SUM across ranks)
+        ends[b].record(stream)
+        total_steps += res.steps_sum
+        if best is None or res.best_E < best:
+            best = res.best_E
+    torch.cuda.synchronize()
+    if pg is not None:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    nse = total_steps * (D - 1)  # total_steps already summed over ranks by the merge
+    value = nse / (dev_ms / 1e3)
+
+    # ---- roofline of the walk kernel (one launch per step) ----------------
+    tau = nse * D  # lag-terms; D per NSE
+    achieved_tops = tau * 2 / (dev_ms / 1e3) / 1e12 / max(1, world)  # per GPU: INT ops (1 MAC = 2 ops)
+    peaks = load_peaks()
+    roof = {"bound": "int32", "achieved": achieved_tops, "peak": peaks["int_tops"], "unit": "Tops/s",
+            "frac": achieved_tops / peaks["int_tops"] if peaks["int_tops"] else None,
+            "traffic": peaks.get("traffic_bytes_per_launch"),
+            "peak_source": peaks["int_src"],
+            "algorithmic_unit": "lag-term tau = one (neighbour, even lag) v(2v-C) MAC; D*(D-1) per walk step, "
+                                f"D={D} per NSE; 2 INT32 ops per tau",
+            "tau_per_s_per_gpu": tau / (dev_ms / 1e3) / max(1, world)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic: random starts from device-derived splitmix64 seeds (derive_walk_seed)",
+        "config": {"workload": f"L={L} throughput: {Wg} walks/GPU/batch, walk_factor {args.walk_factor}, "
+                               f"master_seed {args.master_seed}",
+                   "L": L, "n": n, "walkers_per_gpu": Wg, "global_walkers": Wg * world,
+                   "parallelism": f"walker-sharded x{world}", "variant": args.variant,
+                   "l2": "flushed between batches (256 MiB memset); walk state is on-chip"},
+        "walk_steps_per_s": value / (D - 1),
+        "lag_terms_per_s": value * D,
+        "best_E_seen": best,
+        "wall_s": wall,
+        "roofline": roof,
+        "clocks": clocks,
+        "gpu_launches": 3 * args.steps,
+    }
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, lib, rank, world, dev, pg)
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(L, args.walk_factor, args.master_seed, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        dist.destroy_process_group()
+
+
+def e2e(args, lib, rank, world, dev, pg):
+    """NSE/s through the host-buffer drop-in (sk_saw_batch_host)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_15962_b200 import _lib
+    from paper_2210_15962_b200.runner import derive_walk_seed  # noqa: F401
+
+    L = args.length
+    D = (L + 1) // 2
+    nw = (D + 63) // 64
+    n = args.walk_factor * D
+    W = args.e2e_walkers or args.walkers_per_gpu
+    steps = max(1, min(args.steps, 3))
+    seeds = [host_seeds(args.master_seed, 500 + b, rank * W, W) for b in range(steps + 1)]
+    be = np.empty(W, np.int64)
+    bw = np.empty((W, nw), np.uint64)
+    st = np.empty(W, np.int64)
+    dd = np.empty(W, np.uint8)
+
+    def call(s):
+        _lib.check(lib.sk_saw_batch_host(L, n, s.ctypes.data, W, be.ctypes.data, bw.ctypes.data,
+                                         st.ctypes.data, dd.ctypes.data))
+
+    call(seeds[-1])  # warm-up
+    if pg is not None:
+        dist.barrier()
+    total = 0
+    t0 = time.perf_counter()
+    for b in range(steps):
+        call(seeds[b])
+        total += int(st.sum())
+    el = time.perf_counter() - t0
+    t = torch.tensor([el, float(total)], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        tt = t[1:].clone()
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        t[1] = tt[0]
+    el, total = float(t[0]), float(t[1])
+    return {"value": total * (D - 1) / el, "unit": UNIT, "h2d_bytes_per_step": W * 8,
+            "d2h_bytes_per_step": W * (8 + 8 * nw + 8 + 1),
+            "path": "sk_saw_batch_host (drop-in of _kernels.saw_batch, host numpy buffers)",
+            "walkers_per_step": W, "steps": steps}
+
+
+def host_seeds(master, batch, begin, W):
+    """derive_walk_seed vectorised over walkers (runner.py:53-57)."""
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+    def mix(z):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+    with np.errstate(over="ignore"):
+        h = mix(np.uint64(master) ^ np.uint64(0x9E3779B97F4A7C15))
+        h = mix(h ^ np.uint64(batch))
+        w = np.arange(begin, begin + W, dtype=np.uint64)
+        return np.ascontiguousarray(mix(h ^ w) & M)
+
+
+def load_peaks():
+    """INT32 peak: profiles/microbench (measured on B200 by tools/microbench.cu)
+    if present, else the theoretical 64 IMAD lanes/clk/SM x 148 x 1.965 GHz."""
+    out = {"int_tops": 2 * 148 * 64 * 1.965e9 / 1e12, "int_src": "theoretical IMAD 64 lanes/clk/SM x 148 SM x 1965 MHz (x2 ops)"}
+    p = os.path.join(ROOT, "profiles", "microbench_peaks.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            mb = json.load(f)
+        if mb.get("imad_tops"):
+            out["int_tops"] = mb["imad_tops"]
+            out["int_src"] = f"measured IMAD (profiles/microbench_peaks.json, {mb.get('when', '')})"
+        if mb.get("traffic_bytes_per_launch") is not None:
+            out["traffic_bytes_per_launch"] = mb["traffic_bytes_per_launch"]
+    return out
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_native(a)

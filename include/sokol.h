@@ -1,0 +1,124 @@
+/*
+ * sokol.h -- C ABI of libsokol.so, the B200 (sm_100a) self-avoiding-walk
+ * engine for skew-symmetric LABS (arXiv 2210.15962, "sokol_skew").
+ *
+ * This is the drop-in boundary for the reference's hot path, the numba
+ * kernels in /root/reference/pkg/src/skewsaw/_kernels.py.  Each entry point
+ * names the reference interface it replaces (file:line).  Plain pointers and
+ * sizes only; no torch types.  Every call returns SK_OK (0) or a negative
+ * SK_ERR_* code, with a message available from sk_last_error().
+ *
+ * Data conventions (identical to the reference, _kernels.py:1-13):
+ *   L odd, 3 <= L <= SK_MAX_L;  D = (L+1)/2 free spins;  nw = ceil(D/64).
+ *   words: little-endian uint64, bit D-1-h set iff half spin h is -1
+ *          (equals the hex codec integer, codec.py:34-41).
+ *   seeds: per-walk uint64 seeds as produced by derive_walk_seed
+ *          (runner.py:53-57).
+ */
+#ifndef SOKOL_H
+#define SOKOL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+#define SK_MAX_L 1023   /* D <= 512, nw <= 8 */
+#define SK_MAX_WORDS 8
+
+#define SK_OK 0
+#define SK_ERR_ARG (-1)         /* invalid argument (L even / out of range, n < 1, W < 0, null) */
+#define SK_ERR_UNSUPPORTED (-2) /* valid for the reference but beyond SK_MAX_L */
+#define SK_ERR_CUDA (-3)        /* CUDA runtime error (message in sk_last_error) */
+#define SK_ERR_NOMEM (-4)       /* device or host allocation failed */
+
+/* Kernel variants (sk_set_variant).  All produce identical results. */
+#define SK_VARIANT_AUTO 0
+#define SK_VARIANT_SCALAR 1 /* reference-formula scalar evaluator (cross-check) */
+#define SK_VARIANT_FAST 2   /* production evaluator */
+
+/*
+ * Per-batch reduction written by sk_saw_batch (device memory).  The merge of
+ * runner.py:252-256 (lowest energy wins, ties to the lowest walker index) is
+ * a min over min_key = (best_E << 32) | global_walker_index.
+ */
+typedef struct sk_batch_summary {
+    uint64_t min_key;                  /* (best_E << 32) | walker (global index) */
+    int64_t steps_sum;                 /* sum of steps over the batch's walks (runner.py:251) */
+    uint64_t best_words[SK_MAX_WORDS]; /* packed best half of the winning walk */
+} sk_batch_summary;
+
+int sk_abi_version(void);
+const char *sk_last_error(void);
+int sk_max_length(void);
+
+/* Select the evaluator used by subsequent calls (process-global). */
+int sk_set_variant(int variant);
+int sk_get_variant(void);
+
+/*
+ * Batch of independent walks on the current CUDA device, asynchronous on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).
+ * Replaces skewsaw._kernels.saw_batch(length, n, seeds, best_e_out,
+ * best_words_out, steps_out, dead_out)  (_kernels.py:278-287), called by
+ * runner._BatchLoop.run_batch (runner.py:232-256).
+ *
+ *   d_seeds      W device seeds, or NULL: seed[i] is derived on device as
+ *                derive_walk_seed(master_seed, batch, walker_begin + i).
+ *   d_best_e, d_best_words [W*nw], d_steps, d_dead:  per-walk outputs in
+ *                device memory; each may be NULL (throughput mode).
+ *   d_summary    device sk_batch_summary, or NULL.  Overwritten (not
+ *                accumulated) by this call; walker indices in min_key are
+ *                global (walker_begin + i).
+ */
+int sk_saw_batch(int L, int n, const uint64_t *d_seeds, uint64_t master_seed, uint64_t batch,
+                 uint64_t walker_begin, int64_t W, int64_t *d_best_e, uint64_t *d_best_words,
+                 int64_t *d_steps, uint8_t *d_dead, sk_batch_summary *d_summary, void *stream);
+
+/*
+ * Traced batch: as sk_saw_batch plus the trajectory record of
+ * _kernels.py:231-243, 267-270 (record=True), device memory:
+ *   d_trace_words  [W][n+1][nw]  pivot after t moves (row 0 = first pivot)
+ *   d_trace_deltas [W][n][D]     raw delta vector evaluated at pivot t
+ *                                (a dead walk records one extra row)
+ * Rows beyond a walk's steps (+1 if dead) are left untouched.
+ */
+int sk_saw_trace(int L, int n, const uint64_t *d_seeds, int64_t W, int64_t *d_best_e,
+                 uint64_t *d_best_words, int64_t *d_steps, uint8_t *d_dead,
+                 uint64_t *d_trace_words, int64_t *d_trace_deltas, void *stream);
+
+/*
+ * Host-buffer drop-in of skewsaw._kernels.saw_batch (_kernels.py:278-287):
+ * identical argument list and meaning (host C-contiguous arrays, outputs
+ * written in place).  Copies seeds in, runs on the current device, copies
+ * outputs back, synchronises.  This is the call a ctypes binding of the
+ * reference's batch kernel makes.
+ */
+int sk_saw_batch_host(int L, int n, const uint64_t *seeds, int64_t W, int64_t *best_e_out,
+                      uint64_t *best_words_out, int64_t *steps_out, uint8_t *dead_out);
+
+/*
+ * Host-buffer drop-in of skewsaw._kernels.saw_walk(length, n, seed,
+ * best_words, trace_words, trace_deltas, record) -> (best_e, steps, dead)
+ * (_kernels.py:189-275, called by saw._walk, saw.py:104-130).
+ * trace_words [n+1][nw] and trace_deltas [n][D] are read only if record != 0.
+ */
+int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t *best_words, uint64_t *trace_words,
+                     int64_t *trace_deltas, int record, int64_t *best_e_out, int64_t *steps_out,
+                     uint8_t *dead_out);
+
+/*
+ * Device count of resident walk slots the batch kernel uses for (L, n) on the
+ * current device (persistent grid size in warps).  Informational.
+ */
+int64_t sk_resident_walks(int L, int n);
+
+/* Release the library's cached device buffers (safe to call at any time). */
+int sk_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOKOL_H */

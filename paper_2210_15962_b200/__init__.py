@@ -1,0 +1,32 @@
+"""B200-native sokol_skew: parallel self-avoiding walks for skew-symmetric LABS.
+
+Drop-in for the hot path of the reference package ``skewsaw`` (arXiv
+2210.15962): the walk engine (``_kernels.saw_batch`` / ``saw_walk``), the
+walk API (``saw``) and the solver loop (``runner``), with the same names,
+argument meaning, validation and result records.  Walks run on sm_100a CUDA
+kernels in ``libsokol.so`` (C ABI: include/sokol.h) loaded through ctypes;
+there is no CPU execution path.
+"""
+
+from .codec import DecodeError, decode, encode
+from .core import EnergyRecord, energy, expand_skew, half_dim, merit_factor
+from .runner import (
+    RunConfig,
+    RunRecord,
+    SampleSet,
+    derive_repetition_seed,
+    derive_walk_seed,
+    solve,
+    target_campaign,
+    throughput_report,
+)
+from .saw import WalkConfig, WalkResult, WalkTrace, key, run_walk, run_walk_traced
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DecodeError", "decode", "encode", "EnergyRecord", "energy", "expand_skew", "half_dim",
+    "merit_factor", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
+    "derive_walk_seed", "solve", "target_campaign", "throughput_report", "WalkConfig",
+    "WalkResult", "WalkTrace", "key", "run_walk", "run_walk_traced",
+]

@@ -1,0 +1,87 @@
+"""Drop-in replacement for ``skewsaw._kernels``' walk entry points.
+
+Same names, argument order, dtypes and in-place output semantics as the
+reference's numba kernels, executed by libsokol.so on the current CUDA device:
+
+    saw_batch(length, n, seeds, best_e_out, best_words_out, steps_out, dead_out)
+        -> skewsaw._kernels.saw_batch   (_kernels.py:278-287)
+    saw_walk(length, n, seed, best_words, trace_words, trace_deltas, record)
+        -> skewsaw._kernels.saw_walk    (_kernels.py:189-275)
+    key_of_words(words)
+        -> skewsaw._kernels.key_of_words (_kernels.py:46-53)
+
+Unlike numba, the C ABI validates its arguments and raises ``SokolError``
+(a RuntimeError) on bad input or a CUDA failure.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+MASK64 = (1 << 64) - 1
+KEY_SEED = 0xA0761D6478BD642F
+GOLDEN = 0x9E3779B97F4A7C15
+
+
+def mix64(z: int) -> int:
+    """splitmix64 finaliser on Python ints (_kernels.py:32-37)."""
+    z &= MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def key_of_words(words) -> np.uint64:
+    """Chained key of packed words; host utility (not on the batch path)."""
+    h = KEY_SEED
+    for w in np.asarray(words, dtype=np.uint64).ravel():
+        h = mix64(h ^ int(w))
+    return np.uint64(h)
+
+
+def _req(arr, dtype, name, shape=None):
+    if not isinstance(arr, np.ndarray) or arr.dtype != dtype or not arr.flags.c_contiguous:
+        raise TypeError(f"{name} must be a C-contiguous numpy array of {np.dtype(dtype).name}")
+    if shape is not None and arr.shape != shape:
+        raise ValueError(f"{name} has shape {arr.shape}, expected {shape}")
+    return arr.ctypes.data
+
+
+def saw_batch(length, n, seeds, best_e_out, best_words_out, steps_out, dead_out):
+    """Run one independent walk per seed on the GPU; outputs written in place."""
+    length = int(length)
+    n = int(n)
+    d = (length + 1) // 2
+    nw = (d + 63) // 64
+    W = int(np.asarray(seeds).shape[0])
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    p_seeds = seeds.ctypes.data
+    p_e = _req(best_e_out, np.int64, "best_e_out", (W,))
+    p_w = _req(best_words_out, np.uint64, "best_words_out", (W, nw))
+    p_s = _req(steps_out, np.int64, "steps_out", (W,))
+    p_d = _req(dead_out, np.uint8, "dead_out", (W,))
+    _lib.check(_lib.load().sk_saw_batch_host(length, n, p_seeds, W, p_e, p_w, p_s, p_d))
+
+
+def saw_walk(length, n, seed, best_words, trace_words, trace_deltas, record):
+    """One walk; returns (best_e, steps, dead) like the reference."""
+    length = int(length)
+    n = int(n)
+    d = (length + 1) // 2
+    nw = (d + 63) // 64
+    p_bw = _req(best_words, np.uint64, "best_words", (nw,))
+    if record:
+        p_tw = _req(trace_words, np.uint64, "trace_words", (n + 1, nw))
+        p_td = _req(trace_deltas, np.int64, "trace_deltas", (n, d))
+    else:
+        p_tw = p_td = None
+    be = np.zeros(1, np.int64)
+    st = np.zeros(1, np.int64)
+    dd = np.zeros(1, np.uint8)
+    _lib.check(_lib.load().sk_saw_walk_host(
+        length, n, int(seed) & MASK64, p_bw, p_tw, p_td, 1 if record else 0,
+        be.ctypes.data, st.ctypes.data, dd.ctypes.data,
+    ))
+    return np.int64(be[0]), np.int64(st[0]), bool(dd[0])

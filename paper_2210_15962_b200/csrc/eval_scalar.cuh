@@ -1,0 +1,73 @@
+// eval_scalar.cuh -- reference-formula neighbourhood evaluator (cross-check
+// variant, SK_VARIANT_SCALAR).
+//
+// Lane-per-neighbour evaluation of exactly the arithmetic of neighbor_delta
+// (_kernels.py:85-123) and apply_neighbor (_kernels.py:126-158), on int8
+// spins in shared memory (zero padded, so the reference's range guards are
+// implicit) and int32 even-lag correlations.  O(L) per neighbour; kept as an
+// independent on-device implementation that the production evaluator is
+// cross-checked against in tests (identical traces).
+#pragma once
+#include "walk_engine.cuh"
+
+namespace sk {
+
+__device__ __forceinline__ int32_t pair_products(const int8_t* s, int p, int q, int k) {
+  // Sum of the (up to) four products of _kernels.py:112-121 at lag k; the
+  // range guards are the zero padding, the p+k != q / q-k != p guards are the
+  // single lag k == q - p.
+  const int32_t sp = s[p], sq = s[q];
+  const bool ex = (k == q - p);
+  int32_t t = int32_t(s[p - k]) * sp + sq * int32_t(s[q + k]);
+  if (!ex) t += sp * int32_t(s[p + k]) + int32_t(s[q - k]) * sq;
+  return t;
+}
+
+__device__ __forceinline__ int32_t center_products(const int8_t* s, int p, int k) {
+  const int32_t sp = s[p];  // _kernels.py:98-106
+  return sp * int32_t(s[p + k]) + int32_t(s[p - k]) * sp;
+}
+
+struct EvalScalar {
+  static constexpr uint32_t ext_bytes(int, int) { return 0; }
+
+  __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
+
+  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem& sm, const int8_t* s, int lane) {
+    const int L = P.L, D = P.D;
+    for (int h = lane; h < D; h += 32) {
+      const int p = h, q = L - 1 - h;
+      int32_t acc = 0;
+      if (p == q) {
+        for (int k = 2; k < L; k += 2) {
+          const int32_t d = -2 * center_products(s, p, k);
+          acc += d * (2 * sm.ce[k >> 1] + d);
+        }
+      } else {
+        for (int k = 2; k < L; k += 2) {
+          const int32_t d = -2 * pair_products(s, p, q, k);
+          acc += d * (2 * sm.ce[k >> 1] + d);
+        }
+      }
+      sm.dl[h] = acc;
+    }
+  }
+
+  __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem& sm, int8_t* s, int hs, int lane) {
+    const int L = P.L, K = P.K;
+    const int p = hs, q = L - 1 - hs;
+    for (int j = 1 + lane; j <= K; j += 32) {
+      const int k = 2 * j;
+      const int32_t d = (p == q) ? -center_products(s, p, k) : -pair_products(s, p, q, k);
+      sm.ce[j] += 2 * d;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      s[p] = int8_t(-s[p]);
+      if (p != q) s[q] = int8_t(-s[q]);
+    }
+    __syncwarp();
+  }
+};
+
+}  // namespace sk

@@ -1,0 +1,352 @@
+// sokol_abi.cu -- C ABI of libsokol.so (declared in include/sokol.h).
+//
+// Host side of the drop-in boundary: argument validation (the reference's
+// RunConfig / WalkConfig rules, runner.py:81-97, saw.py:49-55), launch
+// geometry (persistent grid sized from the occupancy calculator, a multiple
+// of the SM count), per-device cached scratch, and the host-buffer entry
+// points that mirror _kernels.saw_batch / saw_walk argument for argument.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sokol.h"
+#include "eval_scalar.cuh"
+#include "eval_fast.cuh"
+#include "walk_engine.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+int g_variant = SK_VARIANT_AUTO;
+std::mutex g_mu;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SK_CUDA(call)                                                                        \
+  do {                                                                                       \
+    cudaError_t _e = (call);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(SK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+struct DevCache {
+  void* gkeys = nullptr;
+  size_t gkeys_bytes = 0;
+  void* words = nullptr;
+  size_t words_bytes = 0;
+  // host-API staging
+  void* h_in = nullptr;
+  size_t h_in_bytes = 0;
+  void* h_out = nullptr;
+  size_t h_out_bytes = 0;
+};
+std::vector<DevCache> g_cache;
+
+int grow(void** p, size_t* have, size_t need) {
+  if (*have >= need) return SK_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  if (cudaMalloc(p, need) != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return fail(SK_ERR_NOMEM, "cudaMalloc of " + std::to_string(need) + " bytes failed");
+  }
+  *have = need;
+  return SK_OK;
+}
+
+DevCache& cache_for(int dev) {
+  if (int(g_cache.size()) <= dev) g_cache.resize(dev + 1);
+  return g_cache[dev];
+}
+
+int validate(int L, int n, int64_t W) {
+  if (L < 3 || (L % 2) == 0) return fail(SK_ERR_ARG, "length must be odd and >= 3, got " + std::to_string(L));
+  if (L > SK_MAX_L)
+    return fail(SK_ERR_UNSUPPORTED, "length " + std::to_string(L) + " exceeds SK_MAX_L=" + std::to_string(SK_MAX_L));
+  if (n < 1) return fail(SK_ERR_ARG, "walk step count n must be >= 1");
+  if (W < 0) return fail(SK_ERR_ARG, "walker count must be >= 0");
+  return SK_OK;
+}
+
+uint32_t visited_capacity(int n) {
+  // strictly larger than the n+1 keys a walk can insert, load <= 15/16
+  const uint64_t need = std::max<uint64_t>(32, (uint64_t(n) + 1) * 16 / 15 + 1);
+  uint32_t cap = 32;
+  while (cap < need) cap <<= 1;
+  return cap;
+}
+
+constexpr int kWPB = 4;                  // warps per block (one walk per warp)
+constexpr uint32_t kSmemKeysMax = 32768;  // keys in smem up to 32 KB per walk
+
+struct Plan {
+  sk::WalkParams P;
+  sk::SmemLayout lay;
+  bool keys_in_smem;
+  int nw;
+};
+
+template <class Eval>
+Plan make_plan(int L, int n) {
+  Plan pl{};
+  const int D = (L + 1) / 2;
+  pl.nw = (D + 63) / 64;
+  pl.P.L = L;
+  pl.P.n = n;
+  pl.P.D = D;
+  pl.P.K = D - 1;
+  pl.P.cap = visited_capacity(n);
+  pl.keys_in_smem = pl.P.cap * 8u <= kSmemKeysMax;
+  pl.lay = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, pl.keys_in_smem, Eval::ext_bytes(L, D));
+  pl.P.warp_smem = pl.lay.total;
+  return pl;
+}
+
+template <int NW, bool TRACE, class Eval>
+int launch_nw(Plan& pl, cudaStream_t st, int dev) {
+  auto kern = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB>;
+  const size_t smem = size_t(pl.P.warp_smem) * kWPB;
+  SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int sms = 0, per_sm = 0;
+  SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem));
+  if (per_sm < 1) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM (smem " + std::to_string(smem) + ")");
+  const int64_t want = (pl.P.W + kWPB - 1) / kWPB;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms));
+  if (!pl.keys_in_smem) {
+    DevCache& c = cache_for(dev);
+    int rc = grow(&c.gkeys, &c.gkeys_bytes, size_t(grid) * kWPB * pl.P.cap * 8u);
+    if (rc) return rc;
+    pl.P.gkeys = static_cast<uint64_t*>(c.gkeys);
+  } else {
+    pl.P.gkeys = nullptr;
+  }
+  kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, pl.lay);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+template <bool TRACE, class Eval>
+int launch_eval(Plan& pl, cudaStream_t st, int dev) {
+  switch (pl.nw) {
+    case 1: return launch_nw<1, TRACE, Eval>(pl, st, dev);
+    case 2: return launch_nw<2, TRACE, Eval>(pl, st, dev);
+    case 3: return launch_nw<3, TRACE, Eval>(pl, st, dev);
+    case 4: return launch_nw<4, TRACE, Eval>(pl, st, dev);
+    case 5: return launch_nw<5, TRACE, Eval>(pl, st, dev);
+    case 6: return launch_nw<6, TRACE, Eval>(pl, st, dev);
+    case 7: return launch_nw<7, TRACE, Eval>(pl, st, dev);
+    case 8: return launch_nw<8, TRACE, Eval>(pl, st, dev);
+  }
+  return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
+}
+
+template <bool TRACE>
+int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, uint64_t walker_begin, int64_t W,
+        int64_t* best_e, uint64_t* best_words, int64_t* steps, uint8_t* dead, sk_batch_summary* summary,
+        uint64_t* trace_words, int64_t* trace_deltas, cudaStream_t st) {
+  int rc = validate(L, n, W);
+  if (rc) return rc;
+  if (summary && walker_begin + uint64_t(W) > (uint64_t(1) << 32))
+    return fail(SK_ERR_ARG, "walker_begin + W must be < 2^32 when a summary is requested");
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast>(L, n);
+  pl.P.seeds = seeds;
+  pl.P.master = master;
+  pl.P.batch = batch;
+  pl.P.walker_begin = walker_begin;
+  pl.P.W = W;
+  pl.P.best_e = best_e;
+  pl.P.steps_out = steps;
+  pl.P.dead_out = dead;
+  pl.P.summary = summary;
+  pl.P.trace_words = trace_words;
+  pl.P.trace_deltas = trace_deltas;
+  pl.P.best_words = best_words;
+  if (summary && !best_words && W > 0) {
+    DevCache& c = cache_for(dev);
+    rc = grow(&c.words, &c.words_bytes, size_t(W) * pl.nw * 8u);
+    if (rc) return rc;
+    pl.P.best_words = static_cast<uint64_t*>(c.words);
+  }
+  if (summary) {
+    sk::summary_init_kernel<<<1, 32, 0, st>>>(summary);
+    SK_CUDA(cudaGetLastError());
+  }
+  if (W > 0) {
+    rc = scalar ? launch_eval<TRACE, sk::EvalScalar>(pl, st, dev) : launch_eval<TRACE, sk::EvalFast>(pl, st, dev);
+    if (rc) return rc;
+  }
+  if (summary && W > 0) {
+    sk::summary_finish_kernel<<<1, 32, 0, st>>>(summary, pl.P.best_words, pl.nw, walker_begin);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+const char* sk_last_error(void) { return g_err.c_str(); }
+int sk_max_length(void) { return SK_MAX_L; }
+
+int sk_set_variant(int v) {
+  if (v != SK_VARIANT_AUTO && v != SK_VARIANT_SCALAR && v != SK_VARIANT_FAST)
+    return fail(SK_ERR_ARG, "unknown variant " + std::to_string(v));
+  g_variant = v;
+  return SK_OK;
+}
+int sk_get_variant(void) { return g_variant; }
+
+int sk_saw_batch(int L, int n, const uint64_t* d_seeds, uint64_t master_seed, uint64_t batch, uint64_t walker_begin,
+                 int64_t W, int64_t* d_best_e, uint64_t* d_best_words, int64_t* d_steps, uint8_t* d_dead,
+                 sk_batch_summary* d_summary, void* stream) {
+  return run<false>(L, n, d_seeds, master_seed, batch, walker_begin, W, d_best_e, d_best_words, d_steps, d_dead,
+                    d_summary, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int sk_saw_trace(int L, int n, const uint64_t* d_seeds, int64_t W, int64_t* d_best_e, uint64_t* d_best_words,
+                 int64_t* d_steps, uint8_t* d_dead, uint64_t* d_trace_words, int64_t* d_trace_deltas, void* stream) {
+  if (!d_seeds || !d_trace_words || !d_trace_deltas) return fail(SK_ERR_ARG, "sk_saw_trace needs seeds and trace buffers");
+  return run<true>(L, n, d_seeds, 0, 0, 0, W, d_best_e, d_best_words, d_steps, d_dead, nullptr, d_trace_words,
+                   d_trace_deltas, static_cast<cudaStream_t>(stream));
+}
+
+int sk_saw_batch_host(int L, int n, const uint64_t* seeds, int64_t W, int64_t* best_e_out, uint64_t* best_words_out,
+                      int64_t* steps_out, uint8_t* dead_out) {
+  int rc = validate(L, n, W);
+  if (rc) return rc;
+  if (W == 0) return SK_OK;
+  if (!seeds || !best_e_out || !best_words_out || !steps_out || !dead_out)
+    return fail(SK_ERR_ARG, "sk_saw_batch_host: null buffer");
+  const int D = (L + 1) / 2, nw = (D + 63) / 64;
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  const size_t in_b = size_t(W) * 8;
+  const size_t o_e = 0, o_w = o_e + size_t(W) * 8, o_s = o_w + size_t(W) * nw * 8, o_d = o_s + size_t(W) * 8;
+  const size_t out_b = o_d + size_t(W);
+  char *din, *dout;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCache& c = cache_for(dev);
+    rc = grow(&c.h_in, &c.h_in_bytes, in_b);
+    if (rc) return rc;
+    rc = grow(&c.h_out, &c.h_out_bytes, out_b);
+    if (rc) return rc;
+    din = static_cast<char*>(c.h_in);
+    dout = static_cast<char*>(c.h_out);
+  }
+  cudaStream_t st = 0;
+  SK_CUDA(cudaMemcpyAsync(din, seeds, in_b, cudaMemcpyHostToDevice, st));
+  rc = run<false>(L, n, reinterpret_cast<const uint64_t*>(din), 0, 0, 0, W, reinterpret_cast<int64_t*>(dout + o_e),
+                  reinterpret_cast<uint64_t*>(dout + o_w), reinterpret_cast<int64_t*>(dout + o_s),
+                  reinterpret_cast<uint8_t*>(dout + o_d), nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
+  SK_CUDA(cudaMemcpyAsync(best_e_out, dout + o_e, size_t(W) * 8, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(best_words_out, dout + o_w, size_t(W) * nw * 8, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(steps_out, dout + o_s, size_t(W) * 8, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(dead_out, dout + o_d, size_t(W), cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaStreamSynchronize(st));
+  return SK_OK;
+}
+
+int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t* best_words, uint64_t* trace_words, int64_t* trace_deltas,
+                     int record, int64_t* best_e_out, int64_t* steps_out, uint8_t* dead_out) {
+  int rc = validate(L, n, 1);
+  if (rc) return rc;
+  if (!best_words || !best_e_out || !steps_out || !dead_out) return fail(SK_ERR_ARG, "sk_saw_walk_host: null buffer");
+  if (record && (!trace_words || !trace_deltas)) return fail(SK_ERR_ARG, "sk_saw_walk_host: record needs trace buffers");
+  const int D = (L + 1) / 2, nw = (D + 63) / 64;
+  const size_t tw_b = record ? size_t(n + 1) * nw * 8 : 0, td_b = record ? size_t(n) * D * 8 : 0;
+  char* buf = nullptr;
+  const size_t o_seed = 0, o_e = 8, o_s = 16, o_d = 24, o_w = 32, o_tw = o_w + size_t(nw) * 8, o_td = o_tw + tw_b;
+  SK_CUDA(cudaMalloc(&buf, o_td + td_b));
+  cudaStream_t st = 0;
+  auto cleanup = [&]() { cudaFree(buf); };
+  if (cudaMemcpyAsync(buf + o_seed, &seed, 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    cleanup();
+    return fail(SK_ERR_CUDA, "seed copy failed");
+  }
+  if (record) {
+    rc = run<true>(L, n, reinterpret_cast<uint64_t*>(buf + o_seed), 0, 0, 0, 1, reinterpret_cast<int64_t*>(buf + o_e),
+                   reinterpret_cast<uint64_t*>(buf + o_w), reinterpret_cast<int64_t*>(buf + o_s),
+                   reinterpret_cast<uint8_t*>(buf + o_d), nullptr, reinterpret_cast<uint64_t*>(buf + o_tw),
+                   reinterpret_cast<int64_t*>(buf + o_td), st);
+  } else {
+    rc = run<false>(L, n, reinterpret_cast<uint64_t*>(buf + o_seed), 0, 0, 0, 1, reinterpret_cast<int64_t*>(buf + o_e),
+                    reinterpret_cast<uint64_t*>(buf + o_w), reinterpret_cast<int64_t*>(buf + o_s),
+                    reinterpret_cast<uint8_t*>(buf + o_d), nullptr, nullptr, nullptr, st);
+  }
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  bool ok = cudaMemcpyAsync(best_e_out, buf + o_e, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaMemcpyAsync(steps_out, buf + o_s, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaMemcpyAsync(dead_out, buf + o_d, 1, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaMemcpyAsync(best_words, buf + o_w, size_t(nw) * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+  if (ok && record) {
+    // rows past the walk's end are left untouched by the kernel: copy only
+    // what was written so that caller-initialised rows survive (saw.py:108-110)
+    ok = cudaStreamSynchronize(st) == cudaSuccess;
+    if (ok) {
+      const int64_t rows_w = *steps_out + 1, rows_d = *steps_out + (*dead_out ? 1 : 0);
+      ok = cudaMemcpyAsync(trace_words, buf + o_tw, size_t(rows_w) * nw * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+           cudaMemcpyAsync(trace_deltas, buf + o_td, size_t(rows_d) * D * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    }
+  }
+  ok = ok && cudaStreamSynchronize(st) == cudaSuccess;
+  cleanup();
+  if (!ok) return fail(SK_ERR_CUDA, std::string("sk_saw_walk_host: ") + cudaGetErrorString(cudaGetLastError()));
+  return SK_OK;
+}
+
+int64_t sk_resident_walks(int L, int n) {
+  if (validate(L, n, 1)) return -1;
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast>(L, n);
+  const size_t smem = size_t(pl.P.warp_smem) * kWPB;
+  // the occupancy of the NW=1 instantiation is representative (same smem)
+  auto kern = sk::saw_walk_kernel<1, false, sk::EvalScalar, kWPB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem) != cudaSuccess) return -1;
+  return int64_t(per_sm) * sms * kWPB;
+}
+
+int sk_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (size_t d = 0; d < g_cache.size(); d++) {
+    DevCache& c = g_cache[d];
+    if (!c.gkeys && !c.words && !c.h_in && !c.h_out) continue;
+    cudaSetDevice(int(d));
+    if (c.gkeys) cudaFree(c.gkeys);
+    if (c.words) cudaFree(c.words);
+    if (c.h_in) cudaFree(c.h_in);
+    if (c.h_out) cudaFree(c.h_out);
+    c = DevCache{};
+  }
+  cudaSetDevice(cur);
+  return SK_OK;
+}
+
+}  // extern "C"

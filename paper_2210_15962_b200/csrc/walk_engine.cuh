@@ -1,0 +1,253 @@
+// walk_engine.cuh -- warp-per-walk driver of the contiguous self-avoiding walk.
+//
+// One warp runs one walk at a time (persistent grid: warp g runs walks
+// g, g + nwarps, ...).  The driver reproduces saw_walk (_kernels.py:189-275)
+// step for step:
+//   init   : first pivot from the splitmix64 stream (204-209), skew expansion
+//            (62-67), O(L^2) sidelobes (70-82), packed words (214-218),
+//            visited set seeded with key(P1) (220-226), best = P1 (228-233)
+//   step   : all-D delta evaluation (239-243) -> lexicographic (delta, h)
+//            argmin over unvisited neighbours (244-258) -> dead end (259-261)
+//            or move (262-274: apply, e += delta, toggle bit, visited.add,
+//            steps += 1, strict '<' best update)
+// The neighbourhood evaluator is a policy class (Eval) so that the scalar
+// reference-formula evaluator and the production evaluator share every other
+// line of the walk.
+#pragma once
+#include "sokol_common.cuh"
+
+namespace sk {
+
+struct WalkParams {
+  int L, n, D, K;
+  uint32_t cap;             // visited-set capacity (power of two)
+  const uint64_t* seeds;    // nullable -> derive on device
+  uint64_t master, batch, walker_begin;
+  int64_t W;
+  int64_t* best_e;          // nullable
+  uint64_t* best_words;     // nullable (then summary words come from scratch)
+  int64_t* steps_out;       // nullable
+  uint8_t* dead_out;        // nullable
+  sk_batch_summary* summary;  // nullable
+  uint64_t* trace_words;    // TRACE only: [W][n+1][nw]
+  int64_t* trace_deltas;    // TRACE only: [W][n][D]
+  uint64_t* gkeys;          // global visited keys [nwarps][cap] or null (keys in smem)
+  uint32_t warp_smem;       // bytes of dynamic smem per warp
+};
+
+// Per-warp shared-memory carve-up.  Offsets are computed identically on host
+// (sokol_abi.cu) and device.
+struct WarpSmem {
+  int8_t* s8;     // full sequence, zero padded: s8[OFF + i] = s_i, i in [0, L)
+  int32_t* ce;    // ce[j] = C_{2j}, j in [0, K]
+  int32_t* dl;    // current delta vector (D entries)
+  uint32_t* occ;  // visited occupancy bitmap
+  uint64_t* keys; // visited keys (smem or global)
+  void* ext;      // evaluator-private area
+};
+
+__host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+struct SmemLayout {
+  uint32_t off_s8, off_ce, off_dl, off_occ, off_keys, off_ext, total;
+  int span_off;  // OFF: s8 index of position 0
+  __host__ __device__ static SmemLayout make(int L, int K, int D, uint32_t cap, bool keys_in_smem,
+                                             uint32_t ext_bytes) {
+    SmemLayout s;
+    s.span_off = L - 1;
+    uint32_t o = 0;
+    s.off_keys = o;
+    if (keys_in_smem) o += cap * 8u;
+    s.off_s8 = o;
+    o = align_up(o + uint32_t(3 * L), 16);
+    s.off_ce = o;
+    o = align_up(o + 4u * uint32_t(K + 1), 16);
+    s.off_dl = o;
+    o = align_up(o + 4u * uint32_t(D), 16);
+    s.off_occ = o;
+    o = align_up(o + 4u * (cap / 32u), 16);
+    s.off_ext = o;
+    o = align_up(o + ext_bytes, 16);
+    s.total = o;
+    return s;
+  }
+};
+
+constexpr int32_t kExcluded = 0x7fffffff;
+
+template <int NW, bool TRACE, class Eval>
+__device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayout& lay, char* wbase,
+                                             uint64_t* gkeys_warp, int64_t w, int lane) {
+  const int L = P.L, D = P.D, K = P.K, n = P.n;
+  const int OFF = lay.span_off;
+  WarpSmem sm;
+  sm.s8 = reinterpret_cast<int8_t*>(wbase + lay.off_s8);
+  sm.ce = reinterpret_cast<int32_t*>(wbase + lay.off_ce);
+  sm.dl = reinterpret_cast<int32_t*>(wbase + lay.off_dl);
+  sm.occ = reinterpret_cast<uint32_t*>(wbase + lay.off_occ);
+  sm.keys = gkeys_warp ? gkeys_warp : reinterpret_cast<uint64_t*>(wbase + lay.off_keys);
+  sm.ext = wbase + lay.off_ext;
+  int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-(L-1), 2L-2], zero outside [0, L)
+
+  // ---- first pivot (_kernels.py:201-209) --------------------------------
+  const uint64_t seed = P.seeds ? P.seeds[w] : derive_walk_seed(P.master, P.batch, P.walker_begin + uint64_t(w));
+  for (int i = lane; i < 3 * L; i += 32) sm.s8[i] = 0;
+  __syncwarp();
+  for (int h = lane; h < D; h += 32) {
+    const uint64_t z = mix64(seed + uint64_t(h + 1) * kGolden);  // counter form of _next64
+    s[h] = (z >> 63) ? int8_t(-1) : int8_t(1);
+  }
+  __syncwarp();
+  for (int i = 1 + lane; i < D; i += 32) s[D - 1 + i] = (i & 1) ? int8_t(-s[D - 1 - i]) : s[D - 1 - i];
+  __syncwarp();
+
+  // ---- packed words (_kernels.py:214-218) --------------------------------
+  uint64_t words[NW];
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const int b0 = 64 * i + lane, b1 = b0 + 32;
+    const uint32_t lo = __ballot_sync(kFull, b0 < D && s[D - 1 - b0] < 0);
+    const uint32_t hi = __ballot_sync(kFull, b1 < D && s[D - 1 - b1] < 0);
+    words[i] = uint64_t(lo) | (uint64_t(hi) << 32);
+  }
+
+  // ---- sidelobes and energy (_kernels.py:70-82; odd lags vanish) --------
+  int32_t epart = 0;
+  for (int j = lane; j <= K; j += 32) {
+    const int k = 2 * j;
+    int32_t acc = 0;
+    for (int i = 0; i < L - k; i++) acc += int32_t(s[i]) * int32_t(s[i + k]);
+    sm.ce[j] = acc;
+    if (j > 0) epart += acc * acc;
+  }
+  int32_t E = warp_sum_i32(epart);
+  __syncwarp();
+
+  Eval ev;
+  ev.init(P, sm, s, lane);
+
+  // ---- visited set with P1 (_kernels.py:220-226) ------------------------
+  VisitedSet vs{sm.keys, sm.occ, P.cap - 1u};
+  vs.clear(lane);
+  __syncwarp();
+  vs.probe(key_of_words<NW>(words), lane, true);
+
+  int32_t best_e = E;
+  uint64_t best_w[NW];
+#pragma unroll
+  for (int i = 0; i < NW; i++) best_w[i] = words[i];
+  const int nw_rt = (D + 63) >> 6;
+  if (TRACE) {
+    if (lane < nw_rt) {
+      uint64_t v = 0;
+#pragma unroll
+      for (int i = 0; i < NW; i++) if (i == lane) v = words[i];
+      P.trace_words[(int64_t(w) * (n + 1)) * nw_rt + lane] = v;
+    }
+  }
+
+  int steps = 0;
+  bool dead = false;
+  for (int step = 0; step < n; step++) {
+    // ---- neighbourhood (_kernels.py:239-243) ----------------------------
+    ev.evaluate(P, sm, s, lane);
+    __syncwarp();
+    if (TRACE) {
+      int64_t* row = P.trace_deltas + (int64_t(w) * n + step) * D;
+      for (int h = lane; h < D; h += 32) row[h] = sm.dl[h];
+    }
+    // ---- best unvisited neighbour (_kernels.py:244-261) -----------------
+    int hs = -1;
+    for (;;) {
+      uint32_t local = kNoCand;
+      for (int h = lane; h < D; h += 32) {
+        const int32_t d = sm.dl[h];
+        if (d != kExcluded) local = min(local, pack_cand(d, h));
+      }
+      const uint32_t m = warp_min_u32(local);
+      if (m == kNoCand) break;
+      const int hc = cand_h(m);
+      const uint64_t nk = key_of_flipped<NW>(words, D, hc);
+      if (!vs.probe(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
+        hs = hc;
+        break;
+      }
+      if (lane == (hc & 31)) sm.dl[hc] = kExcluded;
+      __syncwarp();
+    }
+    if (hs < 0) {
+      dead = true;
+      break;
+    }
+    // ---- move (_kernels.py:262-274) -------------------------------------
+    const int32_t dsel = sm.dl[hs];
+    __syncwarp();
+    ev.apply(P, sm, s, hs, lane);
+    E += dsel;
+    toggle_half_bit<NW>(words, D, hs);
+    steps += 1;
+    if (TRACE) {
+      if (lane < nw_rt) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int i = 0; i < NW; i++) if (i == lane) v = words[i];
+        P.trace_words[(int64_t(w) * (n + 1) + steps) * nw_rt + lane] = v;
+      }
+    }
+    if (E < best_e) {
+      best_e = E;
+#pragma unroll
+      for (int i = 0; i < NW; i++) best_w[i] = words[i];
+    }
+  }
+
+  // ---- outputs (_kernels.py:283-287) and batch reduction ------------------
+  if (lane == 0) {
+    if (P.best_e) P.best_e[w] = best_e;
+    if (P.steps_out) P.steps_out[w] = steps;
+    if (P.dead_out) P.dead_out[w] = dead ? 1 : 0;
+    if (P.summary) {
+      const uint64_t key = (uint64_t(uint32_t(best_e)) << 32) | uint64_t(uint32_t(P.walker_begin + uint64_t(w)));
+      atomicMin(reinterpret_cast<unsigned long long*>(&P.summary->min_key), (unsigned long long)key);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&P.summary->steps_sum), (unsigned long long)steps);
+    }
+  }
+  if (P.best_words && lane < nw_rt) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++) if (i == lane) v = best_w[i];
+    P.best_words[int64_t(w) * nw_rt + lane] = v;
+  }
+  __syncwarp();
+}
+
+template <int NW, bool TRACE, class Eval, int WPB>
+__global__ void __launch_bounds__(WPB * 32) saw_walk_kernel(WalkParams P, SmemLayout lay) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gwarp = int64_t(blockIdx.x) * WPB + wib;
+  const int64_t nwarps = int64_t(gridDim.x) * WPB;
+  char* wbase = smem_raw + size_t(wib) * P.warp_smem;
+  uint64_t* gkeys = P.gkeys ? P.gkeys + size_t(gwarp) * P.cap : nullptr;
+  for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval>(P, lay, wbase, gkeys, w, lane);
+}
+
+// Summary init / finish (tiny single-warp kernels on the same stream).
+__global__ void summary_init_kernel(sk_batch_summary* s) {
+  if (threadIdx.x == 0) {
+    s->min_key = ~0ull;
+    s->steps_sum = 0;
+  }
+  if (threadIdx.x < SK_MAX_WORDS) s->best_words[threadIdx.x] = 0;
+}
+
+__global__ void summary_finish_kernel(sk_batch_summary* s, const uint64_t* best_words, int nw,
+                                      uint64_t walker_begin) {
+  const uint64_t key = s->min_key;
+  if (key == ~0ull) return;
+  const uint64_t local = uint64_t(uint32_t(key)) - uint32_t(walker_begin);
+  if (threadIdx.x < nw) s->best_words[threadIdx.x] = best_words[local * nw + threadIdx.x];
+}
+
+}  // namespace sk

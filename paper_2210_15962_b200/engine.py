@@ -1,0 +1,158 @@
+"""Device-resident batch engine: the fast path behind ``runner.solve``.
+
+One batch = W independent walks whose seeds are derived ON DEVICE from
+(master_seed, batch, global walker index) -- runner.py:53-57 -- so no
+per-walker host work exists (the reference spends ~2.4 us/walker in Python
+deriving seeds and merging, runner.py:234-256).  Each device reduces its
+walks to an ``sk_batch_summary`` (min over (E << 32 | walker), sum of steps,
+winner's words); the host reads 80 bytes per device per batch.
+
+Sharding: walkers [0, W) are split into contiguous slices, one per device
+(in-process ``devices=[...]``) or per rank (``process_group``, one process per
+GPU over NCCL).  Because seeds use the global walker index and the merge key
+carries it, a batch's result is identical for any device count.  Across
+ranks the exchange is one all-reduce MIN of the key and one all-reduce SUM of
+[steps, winner words (owner contributes, others add 0)] -- a few dozen bytes.
+
+PyTorch is used only for device buffers, streams and torch.distributed.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+SUMMARY_WORDS = _lib.SUMMARY_BYTES // 8  # 10 x uint64
+
+
+@dataclass
+class BatchResult:
+    best_E: int
+    walker: int           # global walker index of the winning walk
+    steps_sum: int
+    best_words: np.ndarray  # uint64[nw]
+
+
+def _slices(W: int, parts: int):
+    base, extra = divmod(W, parts)
+    out, start = [], 0
+    for i in range(parts):
+        cnt = base + (1 if i < extra else 0)
+        out.append((start, cnt))
+        start += cnt
+    return out
+
+
+def decode_summary(raw: np.ndarray, nw: int) -> BatchResult | None:
+    """uint64[10] summary -> BatchResult (None if the slice was empty)."""
+    key = int(raw[0])
+    if key == (1 << 64) - 1:
+        return None
+    steps = int(raw[1])
+    return BatchResult(best_E=key >> 32, walker=key & 0xFFFFFFFF, steps_sum=steps,
+                       best_words=raw[2:2 + nw].astype(np.uint64).copy())
+
+
+def merge_across_ranks(win: BatchResult | None, steps: int, nw: int, process_group, device) -> BatchResult:
+    """Merge per-rank batch results: the runner.py:252-256 rule (lowest E,
+    ties to the lowest global walker) is a MIN over (E << 32 | walker); steps
+    add up; the owner of the winning key contributes its words to a SUM in
+    which every other rank adds zeros.  Two tiny all-reduces per batch."""
+    import torch
+    import torch.distributed as dist
+
+    key = (win.best_E << 32) | win.walker if win is not None else (1 << 63) - 1
+    kt = torch.tensor([key], dtype=torch.int64, device=device)
+    dist.all_reduce(kt, op=dist.ReduceOp.MIN, group=process_group)
+    gkey = int(kt.item())
+    payload = np.zeros(1 + nw, dtype=np.int64)
+    payload[0] = steps
+    if win is not None and ((win.best_E << 32) | win.walker) == gkey:
+        payload[1:] = np.asarray(win.best_words, dtype=np.uint64).view(np.int64)
+    pt = torch.from_numpy(payload).to(device)
+    dist.all_reduce(pt, op=dist.ReduceOp.SUM, group=process_group)
+    pv = pt.cpu().numpy()
+    return BatchResult(gkey >> 32, gkey & 0xFFFFFFFF, int(pv[0]), pv[1:].view(np.uint64).copy())
+
+
+class BatchEngine:
+    """Runs batches of W walks of length n = walk_factor * D on GPU(s)."""
+
+    def __init__(self, L: int, walkers: int, n: int, master_seed: int, devices=None, process_group=None):
+        import torch
+
+        self.torch = torch
+        self.L = int(L)
+        self.n = int(n)
+        self.D = (self.L + 1) // 2
+        self.nw = (self.D + 63) // 64
+        self.W = int(walkers)
+        self.master = int(master_seed)
+        self.pg = process_group
+        lib = _lib.load()
+        self.lib = lib
+        if not torch.cuda.is_available():
+            raise _lib.SokolError(_lib.SK_ERR_CUDA, "no CUDA device visible; the engine has no CPU path")
+        if process_group is not None:
+            import torch.distributed as dist
+
+            self.rank = dist.get_rank(process_group)
+            self.world = dist.get_world_size(process_group)
+            devs = [torch.cuda.current_device()] if devices is None else list(devices)
+            if len(devs) != 1:
+                raise ValueError("with a process group each rank drives exactly one device")
+            begin, cnt = _slices(self.W, self.world)[self.rank]
+            self.parts = [(devs[0], begin, cnt)]
+        else:
+            self.rank, self.world = 0, 1
+            devs = [torch.cuda.current_device()] if devices is None else list(devices)
+            self.parts = [(d, b, c) for d, (b, c) in zip(devs, _slices(self.W, len(devs)))]
+        self.streams = []
+        self.summaries = []
+        for dev, _, _ in self.parts:
+            with torch.cuda.device(dev):
+                self.streams.append(torch.cuda.Stream(device=dev))
+                self.summaries.append(torch.empty(SUMMARY_WORDS, dtype=torch.int64, device=dev))
+        self.host = torch.empty((len(self.parts), SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)
+
+    def launch(self, batch: int):
+        """Enqueue batch `batch` on every local device (asynchronous)."""
+        torch = self.torch
+        for i, (dev, begin, cnt) in enumerate(self.parts):
+            with torch.cuda.device(dev):
+                st = self.streams[i]
+                _lib.check(self.lib.sk_saw_batch(
+                    self.L, self.n, None, self.master, int(batch), int(begin), int(cnt),
+                    None, None, None, None, self.summaries[i].data_ptr(), st.cuda_stream,
+                ))
+                with torch.cuda.stream(st):
+                    self.host[i].copy_(self.summaries[i], non_blocking=True)
+
+    def collect(self) -> BatchResult:
+        """Wait for the launched batch and merge it (across ranks if any)."""
+        torch = self.torch
+        for st in self.streams:
+            st.synchronize()
+        raw = self.host.numpy().view(np.uint64)
+        local = [r for r in (decode_summary(raw[i], self.nw) for i in range(len(self.parts))) if r is not None]
+        steps = sum(r.steps_sum for r in local)
+        win = min(local, key=lambda r: (r.best_E, r.walker)) if local else None
+        if self.pg is None:
+            assert win is not None
+            return BatchResult(win.best_E, win.walker, steps, win.best_words)
+        return self._merge_ranks(win, steps)
+
+    def _merge_ranks(self, win: BatchResult | None, steps: int) -> BatchResult:
+        import torch.distributed as dist
+
+        dev = self.parts[0][0]
+        nccl = dist.get_backend(self.pg) == "nccl"
+        tdev = self.torch.device("cuda", dev) if nccl else self.torch.device("cpu")
+        return merge_across_ranks(win, steps, self.nw, self.pg, tdev)
+
+    def run_batch(self, batch: int) -> BatchResult:
+        self.launch(batch)
+        return self.collect()
