@@ -29,12 +29,18 @@ __device__ __forceinline__ int32_t center_products(const int8_t* s, int p, int k
 }
 
 struct EvalScalar {
+  int32_t* dl = nullptr;
+  int nd = 0;
   static constexpr uint32_t ext_bytes(int, int) { return 0; }
+  static bool supports(int) { return true; }
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 
-  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem& sm, const int8_t* s, int lane) {
+  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem& sm, const int8_t* s, int lane,
+                                           int64_t* trace_row) {
     const int L = P.L, D = P.D;
+    dl = sm.dl;
+    nd = D;
     for (int h = lane; h < D; h += 32) {
       const int p = h, q = L - 1 - h;
       int32_t acc = 0;
@@ -50,7 +56,23 @@ struct EvalScalar {
         }
       }
       sm.dl[h] = acc;
+      if (trace_row) trace_row[h] = acc;
     }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ uint32_t local_min() const {
+    uint32_t local = kNoCand;
+    for (int h = int(threadIdx.x & 31); h < nd; h += 32) {
+      const int32_t d = dl[h];
+      if (d != kExcluded) local = min(local, pack_cand(d, h));
+    }
+    return local;
+  }
+
+  __device__ __forceinline__ void exclude(int h, int lane) {
+    if (lane == (h & 31)) dl[h] = kExcluded;
+    __syncwarp();
   }
 
   __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem& sm, int8_t* s, int hs, int lane) {

@@ -152,6 +152,22 @@ int launch_eval(Plan& pl, cudaStream_t st, int dev) {
 }
 
 template <bool TRACE>
+int launch_fast(Plan& pl, cudaStream_t st, int dev) {
+  // compile-time tile bound MT = ceil(NW/2) covers every L with that word count
+  switch (pl.nw) {
+    case 1: return launch_nw<1, TRACE, sk::EvalFast<1>>(pl, st, dev);
+    case 2: return launch_nw<2, TRACE, sk::EvalFast<1>>(pl, st, dev);
+    case 3: return launch_nw<3, TRACE, sk::EvalFast<2>>(pl, st, dev);
+    case 4: return launch_nw<4, TRACE, sk::EvalFast<2>>(pl, st, dev);
+    case 5: return launch_nw<5, TRACE, sk::EvalFast<3>>(pl, st, dev);
+    case 6: return launch_nw<6, TRACE, sk::EvalFast<3>>(pl, st, dev);
+    case 7: return launch_nw<7, TRACE, sk::EvalFast<4>>(pl, st, dev);
+    case 8: return launch_nw<8, TRACE, sk::EvalFast<4>>(pl, st, dev);
+  }
+  return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
+}
+
+template <bool TRACE>
 int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, uint64_t walker_begin, int64_t W,
         int64_t* best_e, uint64_t* best_words, int64_t* steps, uint8_t* dead, sk_batch_summary* summary,
         uint64_t* trace_words, int64_t* trace_deltas, cudaStream_t st) {
@@ -162,8 +178,8 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
   std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
   SK_CUDA(cudaGetDevice(&dev));
-  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast::supports(L);
-  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast>(L, n);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
   pl.P.seeds = seeds;
   pl.P.master = master;
   pl.P.batch = batch;
@@ -187,7 +203,7 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
     SK_CUDA(cudaGetLastError());
   }
   if (W > 0) {
-    rc = scalar ? launch_eval<TRACE, sk::EvalScalar>(pl, st, dev) : launch_eval<TRACE, sk::EvalFast>(pl, st, dev);
+    rc = scalar ? launch_eval<TRACE, sk::EvalScalar>(pl, st, dev) : launch_fast<TRACE>(pl, st, dev);
     if (rc) return rc;
   }
   if (summary && W > 0) {
@@ -321,8 +337,8 @@ int64_t sk_resident_walks(int L, int n) {
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast::supports(L);
-  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast>(L, n);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
   const size_t smem = size_t(pl.P.warp_smem) * kWPB;
   // the occupancy of the NW=1 instantiation is representative (same smem)
   auto kern = sk::saw_walk_kernel<1, false, sk::EvalScalar, kWPB>;

@@ -75,6 +75,7 @@ __device__ __forceinline__ uint32_t pack_cand(int32_t delta, int h) {
   return (uint32_t(delta / 8 + kBias) << kHBits) | uint32_t(h);
 }
 __device__ __forceinline__ int cand_h(uint32_t key) { return int(key & ((1u << kHBits) - 1)); }
+__device__ __forceinline__ int32_t cand_delta(uint32_t key) { return (int32_t(key >> kHBits) - kBias) * 8; }
 
 // ---------------------------------------------------------------------------
 // Per-walk visited set (_kernels.py:168-186 semantics: exact membership of

@@ -150,38 +150,27 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   bool dead = false;
   for (int step = 0; step < n; step++) {
     // ---- neighbourhood (_kernels.py:239-243) ----------------------------
-    ev.evaluate(P, sm, s, lane);
-    __syncwarp();
-    if (TRACE) {
-      int64_t* row = P.trace_deltas + (int64_t(w) * n + step) * D;
-      for (int h = lane; h < D; h += 32) row[h] = sm.dl[h];
-    }
+    ev.evaluate(P, sm, s, lane, TRACE ? P.trace_deltas + (int64_t(w) * n + step) * D : nullptr);
     // ---- best unvisited neighbour (_kernels.py:244-261) -----------------
     int hs = -1;
+    int32_t dsel = 0;
     for (;;) {
-      uint32_t local = kNoCand;
-      for (int h = lane; h < D; h += 32) {
-        const int32_t d = sm.dl[h];
-        if (d != kExcluded) local = min(local, pack_cand(d, h));
-      }
-      const uint32_t m = warp_min_u32(local);
+      const uint32_t m = warp_min_u32(ev.local_min());
       if (m == kNoCand) break;
       const int hc = cand_h(m);
       const uint64_t nk = key_of_flipped<NW>(words, D, hc);
       if (!vs.probe(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
         hs = hc;
+        dsel = cand_delta(m);
         break;
       }
-      if (lane == (hc & 31)) sm.dl[hc] = kExcluded;
-      __syncwarp();
+      ev.exclude(hc, lane);
     }
     if (hs < 0) {
       dead = true;
       break;
     }
     // ---- move (_kernels.py:262-274) -------------------------------------
-    const int32_t dsel = sm.dl[hs];
-    __syncwarp();
     ev.apply(P, sm, s, hs, lane);
     E += dsel;
     toggle_half_bit<NW>(words, D, hs);

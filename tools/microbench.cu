@@ -35,19 +35,10 @@ __device__ __forceinline__ uint64_t gtime() {
   return t;
 }
 
-// clock probe: one thread per block records (clock64, globaltimer) pairs
-__global__ void k_clock(unsigned long long* out, int spin) {
-  if (threadIdx.x == 0) {
-    long long c0 = clock64();
-    uint64_t t0 = gtime();
-    volatile int x = 0;
-    for (int i = 0; i < spin; i++) x += i;
-    long long c1 = clock64();
-    uint64_t t1 = gtime();
-    if (blockIdx.x == 0) {
-      out[0] = (unsigned long long)(c1 - c0);
-      out[1] = t1 - t0;
-    }
+// clock probe: spin for a fixed number of SM cycles; events give the time
+__global__ void k_clock(unsigned long long cycles) {
+  const long long c0 = clock64();
+  while ((unsigned long long)(clock64() - c0) < cycles) {
   }
 }
 
@@ -171,17 +162,22 @@ __global__ void k_imma(int* out, uint32_t a0) {
   if (s == 1234567) out[0] = s;
 }
 
-// shared-memory LDS.32 bandwidth, conflict-free
+// shared-memory LDS.32 bandwidth, conflict-free (inline PTX: nothing to hoist)
 __global__ void k_lds(uint32_t* out, int stride_mask) {
   __shared__ uint32_t buf[4096];
-  for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = i * 7u;
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = (i * 33u) & 4095u;
   __syncthreads();
   uint32_t x[CH];
 #pragma unroll
   for (int c = 0; c < CH; c++) x[c] = (threadIdx.x + 32 * c) & 4095;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(buf);
   for (int i = 0; i < ITERS; i++) {
 #pragma unroll
-    for (int c = 0; c < CH; c++) x[c] = buf[(x[c] + threadIdx.x) & stride_mask] & 4095u;
+    for (int c = 0; c < CH; c++) {
+      uint32_t v;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 4u * ((x[c] + threadIdx.x) & (uint32_t)stride_mask)));
+      x[c] = v;
+    }
   }
   uint32_t s = 0;
 #pragma unroll
@@ -221,19 +217,15 @@ int main() {
   CK(cudaGetDeviceProperties(&prop, dev));
   uint32_t* d_u;
   CK(cudaMalloc(&d_u, 64));
-  unsigned long long* d_clk;
-  CK(cudaMalloc(&d_clk, 16));
 
   const int threads = 256;
   const int blocks = sms * 8;  // 64 warps/SM
   const double lanes = double(blocks) * threads;
 
-  // SM clock under load: run the IMAD kernel concurrently long enough, probe
-  k_clock<<<sms, 32>>>(d_clk, 2000000);
-  CK(cudaDeviceSynchronize());
-  unsigned long long hc[2];
-  CK(cudaMemcpy(hc, d_clk, 16, cudaMemcpyDeviceToHost));
-  const double mhz = double(hc[0]) / double(hc[1]) * 1e3;
+  // SM clock: a kernel spinning a known cycle count on every SM, timed by events
+  const unsigned long long spin = 400000000ull;
+  const double spin_ms = timeit([&] { k_clock<<<sms, 32>>>(spin); });
+  const double mhz = double(spin) / (spin_ms * 1e-3) / 1e6;
 
   auto rate = [&](double ms, double ops_per_lane) { return lanes * ops_per_lane / (ms * 1e-3); };
   double t;
