@@ -77,17 +77,19 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
 
 template <int MT>  // compile-time max number of 8-column tiles
 struct EvalFast {
+  static constexpr int CPL = 4 * MT;  // lags per lane: K <= 128*MT - 1
   FastGeom G;
   __half* ga;  // G copy 1 (pairs at even x aligned)
   __half* gb;  // G copy 2, shifted by one half (pairs at odd x aligned)
   __half* sp0;
   __half* sp1;
-  uint32_t a_addr;      // shared byte address of this lane's A pair at x0 = 2t - g, m = 0
-  uint32_t b_addr[MT];  // shared byte address of this lane's B pair, m = 0
+  uint32_t a_addr;      // shared byte address of this lane's A pair at x0 = 2t - g, m = MLO
+  uint32_t b_addr[MT];  // shared byte address of this lane's B pair, m = MLO
   int hh[MT][4];        // neighbour index of each accumulator slot, -1 if none
   int32_t R[MT][4];
   uint32_t key[MT][4];
-  uint32_t spneg;  // bit (4*nt+o): s_h < 0 for slot (nt, o)
+  uint32_t spneg;       // bit (4*nt+o): s_h < 0 for slot (nt, o)
+  int32_t ce[CPL];      // C_{2j}, j = 1 + lane + 32 r (lag-owned)
 
   static uint32_t ext_bytes(int L, int) { return fast_geom(L).ext_halves * 2u; }
   static bool supports(int L) { return L >= 3 && L <= SK_MAX_L; }
@@ -104,13 +106,18 @@ struct EvalFast {
     const __half z = __ushort_as_half(0);
     for (uint32_t i = lane; i < G.ext_halves; i += 32) base[i] = z;
     __syncwarp();
-    for (int j = 1 + lane; j <= K; j += 32) write_g(j, sm.ce[j]);
+#pragma unroll
+    for (int r = 0; r < CPL; r++) {
+      const int j = 1 + lane + 32 * r;
+      ce[r] = j <= K ? sm.ce[j] : 0;
+      if (j <= K) write_g(j, ce[r]);
+    }
     for (int i = lane; i < D; i += 32) {
-      sp0[G.SPAD + i] = __int2half_rn(s[2 * i]);              // S_0[i] = s_{2i}
+      sp0[G.SPAD + i] = __int2half_rn(s[2 * i]);                     // S_0[i] = s_{2i}
       if (i < D - 1) sp1[G.SPAD + i] = __int2half_rn(s[2 * i + 1]);  // S_1[i] = s_{2i+1}
     }
     const int g = lane >> 2, t = lane & 3;
-    const int x0 = 2 * t - g;
+    const int x0 = 2 * t - g + 16 * G.MLO;
     a_addr = uint32_t(__cvta_generic_to_shared((g & 1) ? gb + G.GOFF + 1 + x0 : ga + G.GOFF + x0));
     spneg = 0;
 #pragma unroll
@@ -118,7 +125,7 @@ struct EvalFast {
       const int c = 8 * nt + g;
       const int pi = c / G.NB, a = c - pi * G.NB;
       const __half* sb = pi == 0 ? sp0 : (pi == 1 ? sp1 : spz);
-      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * a : 0) + 2 * t));
+      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * (a + G.MLO) : 0) + 2 * t));
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int cc = 8 * nt + 2 * t + (o & 1);
@@ -128,10 +135,8 @@ struct EvalFast {
         const bool ok = nt < G.NT && ppi < 2 && h < D;
         hh[nt][o] = ok ? h : -1;
         int32_t r = 0;
-        if (ok && h < K) {
+        if (ok && h < K)
           for (int j = 1; j <= hp; j++) r += int32_t(s[h - 2 * j]) * int32_t(s[h + 2 * j]);
-          (void)0;
-        }
         R[nt][o] = r;
         if (ok && s[h] < 0) spneg |= 1u << (4 * nt + o);
       }
@@ -150,7 +155,7 @@ struct EvalFast {
     }
   }
 
-  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem& sm, const int8_t* s, int lane,
+  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem&, const int8_t* s, int,
                                            int64_t* trace_row) {
     float accA[MT][4], accB[MT][4];
 #pragma unroll
@@ -158,65 +163,54 @@ struct EvalFast {
 #pragma unroll
       for (int o = 0; o < 4; o++) accA[nt][o] = accB[nt][o] = 0.f;
 
-    // rolling A window: pair(x - 8) of the current m
-    uint32_t pm = lds32(a_addr + 2u * uint32_t(16 * G.MLO - 8));
-    for (int m = G.MLO; m <= G.MHI; m += 2) {
+    // Y = sum_m A_m B_m; A pairs roll along m (pair x-8 of step m is pair x+8 of m-1)
+    uint32_t aa = a_addr, bb[MT];
+#pragma unroll
+    for (int nt = 0; nt < MT; nt++) bb[nt] = b_addr[nt];
+    uint32_t pm = lds32(aa - 16u);
+    const int nm = G.MHI - G.MLO + 1;
+    for (int i = 0; i < nm; i += 2) {
       {
-        const uint32_t p0 = lds32(a_addr + 2u * uint32_t(16 * m));
-        const uint32_t p1 = lds32(a_addr + 2u * uint32_t(16 * m + 8));
+        const uint32_t p0 = lds32(aa), p1 = lds32(aa + 16u);
 #pragma unroll
-        for (int nt = 0; nt < MT; nt++) {
-          if (nt < G.NT) {
-            const uint32_t b0 = lds32(b_addr[nt] + 2u * uint32_t(16 * m));
-            const uint32_t b1 = lds32(b_addr[nt] + 2u * uint32_t(16 * m + 8));
-            mma16816(accA[nt], p0, pm, p1, p0, b0, b1);
-          }
-        }
+        for (int nt = 0; nt < MT; nt++)
+          if (nt == 0 || nt < G.NT) mma16816(accA[nt], p0, pm, p1, p0, lds32(bb[nt]), lds32(bb[nt] + 16u));
         pm = p1;
       }
-      if (m + 1 <= G.MHI) {
-        const int m1 = m + 1;
-        const uint32_t p0 = lds32(a_addr + 2u * uint32_t(16 * m1));
-        const uint32_t p1 = lds32(a_addr + 2u * uint32_t(16 * m1 + 8));
+      if (i + 1 < nm) {
+        const uint32_t p0 = lds32(aa + 32u), p1 = lds32(aa + 48u);
 #pragma unroll
-        for (int nt = 0; nt < MT; nt++) {
-          if (nt < G.NT) {
-            const uint32_t b0 = lds32(b_addr[nt] + 2u * uint32_t(16 * m1));
-            const uint32_t b1 = lds32(b_addr[nt] + 2u * uint32_t(16 * m1 + 8));
-            mma16816(accB[nt], p0, pm, p1, p0, b0, b1);
-          }
-        }
+        for (int nt = 0; nt < MT; nt++)
+          if (nt == 0 || nt < G.NT) mma16816(accB[nt], p0, pm, p1, p0, lds32(bb[nt] + 32u), lds32(bb[nt] + 48u));
         pm = p1;
       }
+      aa += 64u;
+#pragma unroll
+      for (int nt = 0; nt < MT; nt++) bb[nt] += 64u;
     }
 
+    // per-neighbour corrections (branch-free; the centre spin uses its own constants)
     const int K = P.K, D = P.D;
+    const __half* gx = ga + G.GOFF + K;  // gx[-h] = G(K - h) = C_{q-p}; gx[-K] = G(0) = 0
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
-        const int h = hh[nt][o];
-        uint32_t kk = kNoCand;
-        if (h >= 0) {
-          const int32_t X = __float2int_rn(accA[nt][o] + accB[nt][o]);
-          const int32_t sp = ((spneg >> (4 * nt + o)) & 1u) ? -1 : 1;
-          int32_t delta;
-          if (h == K) {  // centre spin: v_k = s_p s_{p-k} only
-            delta = 16 * (h >> 1) - 4 * sp * X;
-          } else {
-            const int32_t sq = ((D - 1 - h) & 1) ? -sp : sp;  // s_{L-1-h} by skew symmetry
-            const int32_t cx = sm.ce[K - h];                    // C_{q-p}
-            const int32_t sx = s[3 * h - 2 * K];                // s_{p-(q-p)}, 0 if < 0
-            const int32_t v2 = (K - 1 - (h & 1)) + 2 * R[nt][o] - 2 * sx * sq;
-            delta = 16 * v2 - 8 * sp * (X - sq * cx);
-          }
-          if (trace_row) trace_row[h] = delta;
-          kk = pack_cand(delta, h);
-        }
-        key[nt][o] = kk;
+        const int h0 = hh[nt][o];
+        const int h = max(h0, 0);
+        const bool centre = (h == K);
+        const int32_t X = __float2int_rn(accA[nt][o] + accB[nt][o]);
+        const int32_t sp = ((spneg >> (4 * nt + o)) & 1u) ? -1 : 1;
+        const int32_t sq = ((D - 1 - h) & 1) ? -sp : sp;  // s_{L-1-h} by skew symmetry
+        const int32_t cx = __half2int_rn(gx[-h]);         // C_{q-p} (0 at the centre)
+        const int32_t sx = centre ? 0 : int32_t(s[3 * h - 2 * K]);  // s_{p-(q-p)}, zero padded
+        const int32_t v2 = centre ? (h >> 1) : (K - 1 - (h & 1)) + 2 * R[nt][o] - 2 * sx * sq;
+        const int32_t xm = centre ? 4 : 8;
+        const int32_t delta = 16 * v2 - xm * sp * (X - sq * cx);
+        if (trace_row && h0 >= 0) trace_row[h0] = delta;
+        key[nt][o] = h0 >= 0 ? uint32_t(((delta >> 3) + kBias) << kHBits) + uint32_t(h) : kNoCand;
       }
     }
-    (void)lane;
   }
 
   __device__ __forceinline__ uint32_t local_min() const {
@@ -236,33 +230,43 @@ struct EvalFast {
         if (hh[nt][o] == h) key[nt][o] = kNoCand;
   }
 
-  __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem& sm, int8_t* s, int hs, int lane) {
+  __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem&, int8_t* s, int hs, int lane) {
     const int L = P.L, K = P.K;
     const int p = hs, q = L - 1 - hs;
     const bool centre = (p == q);
     const int32_t sp = s[p];
     const int32_t sq = s[q];
-    // C_k += -4 v_k(h*) for every even lag (apply_neighbor, _kernels.py:126-158)
-    for (int j = 1 + lane; j <= K; j += 32) {
-      const int k = 2 * j;
-      int32_t v = s[p - k];
-      if (!centre && k != q - p) v += s[p + k];
-      const int32_t c = sm.ce[j] - 4 * sp * v;
-      sm.ce[j] = c;
-      write_g(j, c);
+    const int kx = centre ? -1 : q - p;  // the lag whose p+k term is excluded
+    const int csh = centre ? 1 : 0;      // centre: s_{p+k} = s_{p-k}, so v = (sum) / 2
+    const int32_t sp4 = 4 * sp;
+    // C_k -= 4 v_k(h*) for every even lag (apply_neighbor, _kernels.py:126-158);
+    // lags with v_k = 0 leave C_k and its Toeplitz copies untouched
+#pragma unroll
+    for (int r = 0; r < CPL; r++) {
+      const int j = 1 + lane + 32 * r;
+      const int k = 2 * min(j, K);  // clamped so idle lanes read inside the padded span
+      const int32_t a = s[p - k];
+      const int32_t b = (k == kx) ? 0 : int32_t(s[p + k]);
+      const int32_t v = (a + b) >> csh;
+      if (v != 0 && j <= K) {
+        ce[r] -= sp4 * v;
+        write_g(j, ce[r]);
+      }
     }
-    // R_h: the terms s_x s_{2h-x} with x in {p, q} change sign
+    // R_h: the terms s_x s_{2h-x} with x in {p, q} change sign.  Out-of-range
+    // partners read the zero padding; x = h (own flip) and the centre's
+    // coincident pair are masked.
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int h = hh[nt][o];
-        if (h >= 0 && h < K && ((h ^ p) & 1) == 0) {
-          int32_t r = R[nt][o];
-          if (p != h && 2 * h - p >= 0) r -= 2 * sp * int32_t(s[2 * h - p]);
-          if (!centre && 2 * h - q >= 0) r -= 2 * sq * int32_t(s[2 * h - q]);
-          R[nt][o] = r;
-        }
+        const int hc = max(h, 0);
+        const bool act = h >= 0 && h < K && ((h ^ p) & 1) == 0;
+        const int32_t v1 = (h == p) ? 0 : int32_t(s[2 * hc - p]);
+        const int32_t v2 = centre ? 0 : int32_t(s[2 * hc - q]);
+        const int32_t d = sp * v1 + sq * v2;
+        R[nt][o] -= act ? 2 * d : 0;
         if (h == p) spneg ^= 1u << (4 * nt + o);
       }
     }

@@ -148,6 +148,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
 
   int steps = 0;
   bool dead = false;
+  int last = -1;  // half index of the previous move: N_last = P_{t-1} is visited
   for (int step = 0; step < n; step++) {
     // ---- neighbourhood (_kernels.py:239-243) ----------------------------
     ev.evaluate(P, sm, s, lane, TRACE ? P.trace_deltas + (int64_t(w) * n + step) * D : nullptr);
@@ -158,6 +159,10 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
       const uint32_t m = warp_min_u32(ev.local_min());
       if (m == kNoCand) break;
       const int hc = cand_h(m);
+      if (hc == last) {  // undoing the last move returns to P_{t-1}, whose key is in the set
+        ev.exclude(hc, lane);
+        continue;
+      }
       const uint64_t nk = key_of_flipped<NW>(words, D, hc);
       if (!vs.probe(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
         hs = hc;
@@ -172,6 +177,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
     }
     // ---- move (_kernels.py:262-274) -------------------------------------
     ev.apply(P, sm, s, hs, lane);
+    last = hs;
     E += dsel;
     toggle_half_bit<NW>(words, D, hs);
     steps += 1;
