@@ -56,9 +56,11 @@ __host__ __device__ inline FastGeom fast_geom(int L) {
   g.MHI = g.NI - 1;
   g.GOFF = 16 * (g.NB - 1) + 32;
   g.GLEN = g.GOFF + 16 * g.NI + 32;
+  g.GLEN = (g.GLEN + 31) / 64 * 64 + 32;  // copy 2 sits 16 banks away from copy 1
   g.SPAD = 16 * (g.NB - 1) + 16;
   g.SLEN = g.SPAD + 16 * (g.NI + g.NB) + 32;
-  g.ext_halves = uint32_t(g.GLEN + (g.GLEN + 2) + 3 * g.SLEN);
+  g.SLEN = (g.SLEN + 55) / 64 * 64 + 8;   // S_1 sits 4 banks away from S_0: B loads conflict-free
+  g.ext_halves = uint32_t(g.GLEN + (g.GLEN + 2) + 2 * g.SLEN + ((D + 1) & ~1));
   return g;
 }
 
@@ -75,24 +77,36 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int MT>  // compile-time max number of 8-column tiles
+// MT  : compile-time max number of 8-column tiles (ceil(NW/2) covers every L)
+// NMC : compile-time MMA count per step (even), 0 = runtime (G.nm)
+template <int MT, int NMC = 0>
 struct EvalFast {
   static constexpr int CPL = 4 * MT;  // lags per lane: K <= 128*MT - 1
   FastGeom G;
-  __half* ga;  // G copy 1 (pairs at even x aligned)
-  __half* gb;  // G copy 2, shifted by one half (pairs at odd x aligned)
+  __half* ga;           // G copy 1 (pairs at even x aligned)
+  __half* gb;           // G copy 2, shifted by one half (pairs at odd x aligned)
   __half* sp0;
   __half* sp1;
+  int16_t* ces;         // int16 copy of C_{2j}, read by the epilogue (C_{q-p})
   uint32_t a_addr;      // shared byte address of this lane's A pair at x0 = 2t - g, m = MLO
   uint32_t b_addr[MT];  // shared byte address of this lane's B pair, m = MLO
-  int hh[MT][4];        // neighbour index of each accumulator slot, -1 if none
-  int32_t R[MT][4];
+  // per accumulator slot (nt, o): neighbour h (clamped to >= 0) and its constants
+  int hc[MT][4];
+  uint32_t inv[MT][4];  // 0 for a live slot, ~0 for padding
+  int32_t R[MT][4];     // sum_j s_{h-2j} s_{h+2j}
+  int32_t xsp[MT][4];   // xm * s_h  (xm = 8, 4 at the centre, 0 for padding)
+  int32_t sqv[MT][4];   // s_{L-1-h} (0 at the centre / padding)
+  int32_t c16[MT][4];   // 16 * (K - 1 - pi), 16 * (h >> 1) at the centre
+  int32_t xq[MT][4];    // xm * s_q s_p (= +-8; 0 at the centre / padding)
   uint32_t key[MT][4];
-  uint32_t spneg;       // bit (4*nt+o): s_h < 0 for slot (nt, o)
   int32_t ce[CPL];      // C_{2j}, j = 1 + lane + 32 r (lag-owned)
 
   static uint32_t ext_bytes(int L, int) { return fast_geom(L).ext_halves * 2u; }
   static bool supports(int L) { return L >= 3 && L <= SK_MAX_L; }
+  static constexpr bool kNeedsDl = false;
+  static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
+  static constexpr int kMinBlocks = MT == 1 ? 4 : 1;  // <= 128 registers (measured best; 5 spills into LDC)
+  static int span_hi(int L, int D) { return L - 1 + (D - 1); }  // p + 2K
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
     G = fast_geom(P.L);
@@ -102,7 +116,7 @@ struct EvalFast {
     gb = ga + G.GLEN;
     sp0 = gb + G.GLEN + 2;
     sp1 = sp0 + G.SLEN;
-    __half* spz = sp1 + G.SLEN;
+    ces = reinterpret_cast<int16_t*>(sp1 + G.SLEN);
     const __half z = __ushort_as_half(0);
     for (uint32_t i = lane; i < G.ext_halves; i += 32) base[i] = z;
     __syncwarp();
@@ -110,7 +124,10 @@ struct EvalFast {
     for (int r = 0; r < CPL; r++) {
       const int j = 1 + lane + 32 * r;
       ce[r] = j <= K ? sm.ce[j] : 0;
-      if (j <= K) write_g(j, ce[r]);
+      if (j <= K) {
+        write_g(j, ce[r]);
+        ces[j] = int16_t(ce[r]);
+      }
     }
     for (int i = lane; i < D; i += 32) {
       sp0[G.SPAD + i] = __int2half_rn(s[2 * i]);                     // S_0[i] = s_{2i}
@@ -119,12 +136,11 @@ struct EvalFast {
     const int g = lane >> 2, t = lane & 3;
     const int x0 = 2 * t - g + 16 * G.MLO;
     a_addr = uint32_t(__cvta_generic_to_shared((g & 1) ? gb + G.GOFF + 1 + x0 : ga + G.GOFF + x0));
-    spneg = 0;
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
       const int c = 8 * nt + g;
       const int pi = c / G.NB, a = c - pi * G.NB;
-      const __half* sb = pi == 0 ? sp0 : (pi == 1 ? sp1 : spz);
+      const __half* sb = pi == 1 ? sp1 : sp0;  // columns past 2*NB are padding: any signal will do
       b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * (a + G.MLO) : 0) + 2 * t));
 #pragma unroll
       for (int o = 0; o < 4; o++) {
@@ -133,12 +149,19 @@ struct EvalFast {
         const int hp = 16 * aa + g + 8 * (o >> 1);
         const int h = 2 * hp + ppi;
         const bool ok = nt < G.NT && ppi < 2 && h < D;
-        hh[nt][o] = ok ? h : -1;
+        const bool centre = ok && h == K;
+        hc[nt][o] = ok ? h : 0;
+        inv[nt][o] = ok ? 0u : ~0u;
         int32_t r = 0;
-        if (ok && h < K)
+        if (ok && !centre)
           for (int j = 1; j <= hp; j++) r += int32_t(s[h - 2 * j]) * int32_t(s[h + 2 * j]);
         R[nt][o] = r;
-        if (ok && s[h] < 0) spneg |= 1u << (4 * nt + o);
+        const int32_t sp = ok ? int32_t(s[h]) : 0;
+        const int32_t qs = ((D - 1 - h) & 1) ? -1 : 1;  // s_{L-1-h} = qs * s_h (skew symmetry)
+        xsp[nt][o] = (centre ? 4 : 8) * sp;
+        sqv[nt][o] = centre ? 0 : qs * sp;
+        c16[nt][o] = ok ? 16 * (centre ? (h >> 1) : (K - 1 - (h & 1))) : 0;
+        xq[nt][o] = (ok && !centre) ? 8 * qs : 0;
       }
     }
     __syncwarp();
@@ -155,6 +178,14 @@ struct EvalFast {
     }
   }
 
+  __device__ __forceinline__ void mma_pair(float (&acc)[MT][4], uint32_t aa, const uint32_t (&bb)[MT], uint32_t& pm) {
+    const uint32_t p0 = lds32(aa), p1 = lds32(aa + 16u);
+#pragma unroll
+    for (int nt = 0; nt < MT; nt++)
+      if (nt == 0 || nt < G.NT) mma16816(acc[nt], p0, pm, p1, p0, lds32(bb[nt]), lds32(bb[nt] + 16u));
+    pm = p1;
+  }
+
   __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem&, const int8_t* s, int,
                                            int64_t* trace_row) {
     float accA[MT][4], accB[MT][4];
@@ -163,52 +194,51 @@ struct EvalFast {
 #pragma unroll
       for (int o = 0; o < 4; o++) accA[nt][o] = accB[nt][o] = 0.f;
 
-    // Y = sum_m A_m B_m; A pairs roll along m (pair x-8 of step m is pair x+8 of m-1)
+    // Y = sum_m A_m B_m; A pairs roll along m (pair x-8 of step m is pair x+8 of m-1).
+    // The MMA count is padded to even; the extra block reads zero signal.
     uint32_t aa = a_addr, bb[MT];
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) bb[nt] = b_addr[nt];
     uint32_t pm = lds32(aa - 16u);
-    const int nm = G.MHI - G.MLO + 1;
-    for (int i = 0; i < nm; i += 2) {
-      {
-        const uint32_t p0 = lds32(aa), p1 = lds32(aa + 16u);
+    if (NMC > 0) {
 #pragma unroll
-        for (int nt = 0; nt < MT; nt++)
-          if (nt == 0 || nt < G.NT) mma16816(accA[nt], p0, pm, p1, p0, lds32(bb[nt]), lds32(bb[nt] + 16u));
-        pm = p1;
+      for (int i = 0; i < NMC; i += 2) {
+        mma_pair(accA, aa, bb, pm);
+#pragma unroll
+        for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
+        mma_pair(accB, aa + 32u, bb, pm);
+        aa += 64u;
+#pragma unroll
+        for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
       }
-      if (i + 1 < nm) {
-        const uint32_t p0 = lds32(aa + 32u), p1 = lds32(aa + 48u);
+    } else {
+      const int nm = G.MHI - G.MLO + 1;
+      for (int i = 0; i < nm; i += 2) {
+        mma_pair(accA, aa, bb, pm);
 #pragma unroll
-        for (int nt = 0; nt < MT; nt++)
-          if (nt == 0 || nt < G.NT) mma16816(accB[nt], p0, pm, p1, p0, lds32(bb[nt] + 32u), lds32(bb[nt] + 48u));
-        pm = p1;
+        for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
+        mma_pair(accB, aa + 32u, bb, pm);
+        aa += 64u;
+#pragma unroll
+        for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
       }
-      aa += 64u;
-#pragma unroll
-      for (int nt = 0; nt < MT; nt++) bb[nt] += 64u;
     }
 
-    // per-neighbour corrections (branch-free; the centre spin uses its own constants)
-    const int K = P.K, D = P.D;
-    const __half* gx = ga + G.GOFF + K;  // gx[-h] = G(K - h) = C_{q-p}; gx[-K] = G(0) = 0
+    // dE(h) = 16 (c0 + 2R - 2 s_x s_q) - xm s_p (X - s_q C_{q-p})   (see header)
+    const int K = P.K;
+    const int8_t* sx0 = s - 2 * K;   // sx0[3h] = s_{3h-2K} = s_{p-(q-p)} (zero padded)
+    const int16_t* cx0 = ces + K;    // cx0[-h] = C_{q-p}
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
-        const int h0 = hh[nt][o];
-        const int h = max(h0, 0);
-        const bool centre = (h == K);
+        const int h = hc[nt][o];
         const int32_t X = __float2int_rn(accA[nt][o] + accB[nt][o]);
-        const int32_t sp = ((spneg >> (4 * nt + o)) & 1u) ? -1 : 1;
-        const int32_t sq = ((D - 1 - h) & 1) ? -sp : sp;  // s_{L-1-h} by skew symmetry
-        const int32_t cx = __half2int_rn(gx[-h]);         // C_{q-p} (0 at the centre)
-        const int32_t sx = centre ? 0 : int32_t(s[3 * h - 2 * K]);  // s_{p-(q-p)}, zero padded
-        const int32_t v2 = centre ? (h >> 1) : (K - 1 - (h & 1)) + 2 * R[nt][o] - 2 * sx * sq;
-        const int32_t xm = centre ? 4 : 8;
-        const int32_t delta = 16 * v2 - xm * sp * (X - sq * cx);
-        if (trace_row && h0 >= 0) trace_row[h0] = delta;
-        key[nt][o] = h0 >= 0 ? uint32_t(((delta >> 3) + kBias) << kHBits) + uint32_t(h) : kNoCand;
+        const int32_t cx = cx0[-h];
+        const int32_t sx = sx0[3 * h];
+        const int32_t delta = c16[nt][o] + 32 * (R[nt][o] - sx * sqv[nt][o]) - xsp[nt][o] * X + xq[nt][o] * cx;
+        if (trace_row && !inv[nt][o]) trace_row[h] = delta;
+        key[nt][o] = ((uint32_t((delta >> 3) + kBias) << kHBits) + uint32_t(h)) | inv[nt][o];
       }
     }
   }
@@ -227,7 +257,7 @@ struct EvalFast {
     for (int nt = 0; nt < MT; nt++)
 #pragma unroll
       for (int o = 0; o < 4; o++)
-        if (hh[nt][o] == h) key[nt][o] = kNoCand;
+        if (hc[nt][o] == h) key[nt][o] = kNoCand;
   }
 
   __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem&, int8_t* s, int hs, int lane) {
@@ -240,7 +270,7 @@ struct EvalFast {
     const int csh = centre ? 1 : 0;      // centre: s_{p+k} = s_{p-k}, so v = (sum) / 2
     const int32_t sp4 = 4 * sp;
     // C_k -= 4 v_k(h*) for every even lag (apply_neighbor, _kernels.py:126-158);
-    // lags with v_k = 0 leave C_k and its Toeplitz copies untouched
+    // lags with v_k = 0 leave C_k and its copies untouched
 #pragma unroll
     for (int r = 0; r < CPL; r++) {
       const int j = 1 + lane + 32 * r;
@@ -250,24 +280,26 @@ struct EvalFast {
       const int32_t v = (a + b) >> csh;
       if (v != 0 && j <= K) {
         ce[r] -= sp4 * v;
+        ces[j] = int16_t(ce[r]);
         write_g(j, ce[r]);
       }
     }
     // R_h: the terms s_x s_{2h-x} with x in {p, q} change sign.  Out-of-range
     // partners read the zero padding; x = h (own flip) and the centre's
-    // coincident pair are masked.
+    // coincident pair are masked.  A flip of h itself negates s_h and s_{L-1-h}.
+    const int pp = p & 1;
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
-        const int h = hh[nt][o];
-        const int hc = max(h, 0);
-        const bool act = h >= 0 && h < K && ((h ^ p) & 1) == 0;
-        const int32_t v1 = (h == p) ? 0 : int32_t(s[2 * hc - p]);
-        const int32_t v2 = centre ? 0 : int32_t(s[2 * hc - q]);
-        const int32_t d = sp * v1 + sq * v2;
-        R[nt][o] -= act ? 2 * d : 0;
-        if (h == p) spneg ^= 1u << (4 * nt + o);
+        const int h = hc[nt][o];
+        const bool own = (h == p) && !inv[nt][o];
+        const bool act = ((h & 1) == pp) && (sqv[nt][o] != 0);  // live, non-centre, same parity
+        const int32_t v1 = own ? 0 : int32_t(s[2 * h - p]);
+        const int32_t v2 = centre ? 0 : int32_t(s[2 * h - q]);
+        R[nt][o] -= act ? 2 * (sp * v1 + sq * v2) : 0;
+        xsp[nt][o] = own ? -xsp[nt][o] : xsp[nt][o];
+        sqv[nt][o] = own ? -sqv[nt][o] : sqv[nt][o];
       }
     }
     __syncwarp();

@@ -33,6 +33,10 @@ struct EvalScalar {
   int nd = 0;
   static constexpr uint32_t ext_bytes(int, int) { return 0; }
   static bool supports(int) { return true; }
+  static constexpr bool kNeedsDl = true;
+  static constexpr bool kCeAliasKeys = false;
+  static constexpr int kMinBlocks = 1;
+  static int span_hi(int L, int) { return 2 * L - 2; }  // q + k
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 

@@ -107,7 +107,8 @@ Plan make_plan(int L, int n) {
   pl.P.K = D - 1;
   pl.P.cap = visited_capacity(n);
   pl.keys_in_smem = pl.P.cap * 8u <= kSmemKeysMax;
-  pl.lay = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, pl.keys_in_smem, Eval::ext_bytes(L, D));
+  pl.lay = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, pl.keys_in_smem, Eval::ext_bytes(L, D), Eval::kNeedsDl,
+                                Eval::span_hi(L, D), Eval::kCeAliasKeys);
   pl.P.warp_smem = pl.lay.total;
   return pl;
 }
@@ -151,12 +152,28 @@ int launch_eval(Plan& pl, cudaStream_t st, int dev) {
   return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
 }
 
+template <int NW, bool TRACE>
+int launch_fast_small(Plan& pl, cudaStream_t st, int dev) {
+  // one 8-column tile (D <= 128): the per-step MMA count is a compile-time constant
+  const sk::FastGeom g = sk::fast_geom(pl.P.L);
+  const int nm = ((g.MHI - g.MLO + 1) + 1) & ~1;
+  switch (nm) {
+    case 2: return launch_nw<NW, TRACE, sk::EvalFast<1, 2>>(pl, st, dev);
+    case 4: return launch_nw<NW, TRACE, sk::EvalFast<1, 4>>(pl, st, dev);
+    case 6: return launch_nw<NW, TRACE, sk::EvalFast<1, 6>>(pl, st, dev);
+    case 8: return launch_nw<NW, TRACE, sk::EvalFast<1, 8>>(pl, st, dev);
+    case 10: return launch_nw<NW, TRACE, sk::EvalFast<1, 10>>(pl, st, dev);
+    case 12: return launch_nw<NW, TRACE, sk::EvalFast<1, 12>>(pl, st, dev);
+  }
+  return launch_nw<NW, TRACE, sk::EvalFast<1, 0>>(pl, st, dev);
+}
+
 template <bool TRACE>
 int launch_fast(Plan& pl, cudaStream_t st, int dev) {
   // compile-time tile bound MT = ceil(NW/2) covers every L with that word count
   switch (pl.nw) {
-    case 1: return launch_nw<1, TRACE, sk::EvalFast<1>>(pl, st, dev);
-    case 2: return launch_nw<2, TRACE, sk::EvalFast<1>>(pl, st, dev);
+    case 1: return launch_fast_small<1, TRACE>(pl, st, dev);
+    case 2: return launch_fast_small<2, TRACE>(pl, st, dev);
     case 3: return launch_nw<3, TRACE, sk::EvalFast<2>>(pl, st, dev);
     case 4: return launch_nw<4, TRACE, sk::EvalFast<2>>(pl, st, dev);
     case 5: return launch_nw<5, TRACE, sk::EvalFast<3>>(pl, st, dev);

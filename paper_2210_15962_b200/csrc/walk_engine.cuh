@@ -51,19 +51,29 @@ __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x
 struct SmemLayout {
   uint32_t off_s8, off_ce, off_dl, off_occ, off_keys, off_ext, total;
   int span_off;  // OFF: s8 index of position 0
+  uint32_t span;  // s8 bytes
+  // span_hi: highest position index the evaluator reads (scalar: 2L-2, fast: L-1+K).
+  // ce_alias_keys: the int32 C array is only read during init, so it may share
+  // the visited-set key storage (cleared after init) when that is in smem.
   __host__ __device__ static SmemLayout make(int L, int K, int D, uint32_t cap, bool keys_in_smem,
-                                             uint32_t ext_bytes) {
+                                             uint32_t ext_bytes, bool need_dl, int span_hi, bool ce_alias_keys) {
     SmemLayout s;
     s.span_off = L - 1;
+    s.span = uint32_t(L - 1 + span_hi + 1);
+    const bool alias = ce_alias_keys && keys_in_smem && cap * 8u >= 4u * uint32_t(K + 1);
     uint32_t o = 0;
     s.off_keys = o;
     if (keys_in_smem) o += cap * 8u;
     s.off_s8 = o;
-    o = align_up(o + uint32_t(3 * L), 16);
-    s.off_ce = o;
-    o = align_up(o + 4u * uint32_t(K + 1), 16);
+    o = align_up(o + s.span, 16);
+    if (alias) {
+      s.off_ce = s.off_keys;
+    } else {
+      s.off_ce = o;
+      o = align_up(o + 4u * uint32_t(K + 1), 16);
+    }
     s.off_dl = o;
-    o = align_up(o + 4u * uint32_t(D), 16);
+    if (need_dl) o = align_up(o + 4u * uint32_t(D), 16);
     s.off_occ = o;
     o = align_up(o + 4u * (cap / 32u), 16);
     s.off_ext = o;
@@ -87,11 +97,11 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   sm.occ = reinterpret_cast<uint32_t*>(wbase + lay.off_occ);
   sm.keys = gkeys_warp ? gkeys_warp : reinterpret_cast<uint64_t*>(wbase + lay.off_keys);
   sm.ext = wbase + lay.off_ext;
-  int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-(L-1), 2L-2], zero outside [0, L)
+  int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-(L-1), span_hi], zero outside [0, L)
 
   // ---- first pivot (_kernels.py:201-209) --------------------------------
   const uint64_t seed = P.seeds ? P.seeds[w] : derive_walk_seed(P.master, P.batch, P.walker_begin + uint64_t(w));
-  for (int i = lane; i < 3 * L; i += 32) sm.s8[i] = 0;
+  for (int i = lane; i < int(lay.span); i += 32) sm.s8[i] = 0;
   __syncwarp();
   for (int h = lane; h < D; h += 32) {
     const uint64_t z = mix64(seed + uint64_t(h + 1) * kGolden);  // counter form of _next64
@@ -217,7 +227,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
 }
 
 template <int NW, bool TRACE, class Eval, int WPB>
-__global__ void __launch_bounds__(WPB * 32) saw_walk_kernel(WalkParams P, SmemLayout lay) {
+__global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(WalkParams P, SmemLayout lay) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
