@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-walkers", type=int, default=0, help="walkers per e2e step (0 = walkers-per-gpu)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N>1 (gloo lets 2 ranks share one GPU in tests)")
     return ap.parse_args()
 
 
@@ -184,12 +186,17 @@ def run_native(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = local % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     pg = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or "MASTER_ADDR" in os.environ:
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         pg = dist.group.WORLD
+    mdev = dev if args.backend == "nccl" else torch.device("cpu")  # merge tensors live here
     lib = _lib.load()
     _lib.set_variant({"auto": 0, "scalar": 1, "fast": 2}[args.variant])
 
@@ -211,13 +218,13 @@ def run_native(args):
         loc = engine.decode_summary(summ.cpu().numpy().view(np.uint64), nw)
         if pg is None:
             return loc
-        return engine.merge_across_ranks(loc, loc.steps_sum if loc else 0, nw, pg, dev)
+        return engine.merge_across_ranks(loc, loc.steps_sum if loc else 0, nw, pg, mdev)
 
     for b in range(args.warmup):
         launch(1000 + b)
         merge()
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     sampler.start()
     time.sleep(0.3)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -243,7 +250,7 @@ def run_native(args):
     wall = time.perf_counter() - wall0
     clocks = sampler.stop()
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=mdev)
     if pg is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms = float(t.item())
@@ -254,9 +261,11 @@ def run_native(args):
     tau = nse * D  # lag-terms; D per NSE
     achieved_tops = tau * 2 / (dev_ms / 1e3) / 1e12 / max(1, world)  # per GPU: INT ops (1 MAC = 2 ops)
     peaks = load_peaks()
+    ncu = load_ncu(L, Wg)
     roof = {"bound": "int32", "achieved": achieved_tops, "peak": peaks["int_tops"], "unit": "Tops/s",
             "frac": achieved_tops / peaks["int_tops"] if peaks["int_tops"] else None,
-            "traffic": peaks.get("traffic_bytes_per_launch"),
+            "traffic": ncu.get("traffic_bytes_per_launch"),
+            "ncu": ncu,
             "peak_source": peaks["int_src"],
             "algorithmic_unit": "lag-term tau = one (neighbour, even lag) v(2v-C) MAC; D*(D-1) per walk step, "
                                 f"D={D} per NSE; 2 INT32 ops per tau",
@@ -281,7 +290,7 @@ def run_native(args):
         "gpu_launches": 3 * args.steps,
     }
     if not args.no_e2e:
-        line["e2e"] = e2e(args, lib, rank, world, dev, pg)
+        line["e2e"] = e2e(args, lib, rank, world, mdev, pg)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(L, args.walk_factor, args.master_seed, args.cpu_seconds)
     if rank == 0:
@@ -323,13 +332,12 @@ def e2e(args, lib, rank, world, dev, pg):
         call(seeds[b])
         total += int(st.sum())
     el = time.perf_counter() - t0
-    t = torch.tensor([el, float(total)], dtype=torch.float64, device=dev)
     if pg is not None:
-        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
-        tt = t[1:].clone()
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        t[1] = tt[0]
-    el, total = float(t[0]), float(t[1])
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        tn = torch.tensor([float(total)], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tn, op=dist.ReduceOp.SUM)
+        el, total = float(te.item()), float(tn.item())
     return {"value": total * (D - 1) / el, "unit": UNIT, "h2d_bytes_per_step": W * 8,
             "d2h_bytes_per_step": W * (8 + 8 * nw + 8 + 1),
             "path": "sk_saw_batch_host (drop-in of _kernels.saw_batch, host numpy buffers)",
@@ -350,6 +358,22 @@ def host_seeds(master, batch, begin, W):
         h = mix(h ^ np.uint64(batch))
         w = np.arange(begin, begin + W, dtype=np.uint64)
         return np.ascontiguousarray(mix(h ^ w) & M)
+
+
+def load_ncu(L, W):
+    """DRAM traffic and pipe utilisation of the walk kernel from the committed
+    ncu --set full capture of this bench's launch (profiles/ncu_walk_kernel.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_walk_kernel.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        d = json.load(f)
+    out = {k: d[k] for k in ("source", "tensor_pipe_pct", "alu_pipe_pct", "lsu_pipe_pct", "issue_busy_pct",
+                             "warps_per_sm", "registers") if k in d}
+    if d.get("L") == L and d.get("walks") and d.get("dram_bytes") is not None:
+        out["traffic_bytes_per_launch"] = d["dram_bytes"] * (W / d["walks"])
+        out["traffic_note"] = f"dram read+write of one captured launch ({d['walks']} walks), scaled to {W} walks"
+    return out
 
 
 def load_peaks():

@@ -1,0 +1,45 @@
+"""Extract the walk kernel's roofline evidence from an ncu --set full report
+into profiles/ncu_walk_kernel.json (read by bench.py for roofline.traffic).
+
+    python tools/ncu_to_json.py gpurun_out/prof_bench.ncu-rep L WALKS > profiles/ncu_walk_kernel.json
+"""
+import csv
+import json
+import subprocess
+import sys
+
+rep, L, W = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                                     text=True).stdout.splitlines()))
+names, units, vals = raw[0], raw[1], raw[2]
+
+
+def get(key):
+    if key not in names:
+        return None
+    v = vals[names.index(key)].replace(",", "")
+    u = units[names.index(key)]
+    try:
+        x = float(v)
+    except ValueError:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6}.get(u, 1)
+    return x * scale
+
+
+out = {
+    "source": rep.split("/")[-1] + " (ncu --set full --clock-control none, one timed bench launch)",
+    "L": L, "walks": W,
+    "kernel": vals[names.index("Kernel Name")] if "Kernel Name" in names else None,
+    "duration_ns": get("gpu__time_duration.sum"),
+    "dram_bytes": (get("dram__bytes_read.sum") or 0) + (get("dram__bytes_write.sum") or 0),
+    "tensor_pipe_pct": get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+    "alu_pipe_pct": get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+    "fma_pipe_pct": get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+    "lsu_pipe_pct": get("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+    "issue_busy_pct": get("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    "warps_per_sm": get("sm__warps_active.avg.per_cycle_active"),
+    "registers": get("launch__registers_per_thread"),
+    "inst_executed": get("smsp__inst_executed.sum"),
+}
+print(json.dumps(out, indent=1))
