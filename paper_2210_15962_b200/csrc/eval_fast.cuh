@@ -105,7 +105,7 @@ struct EvalFast {
   static bool supports(int L) { return L >= 3 && L <= SK_MAX_L; }
   static constexpr bool kNeedsDl = false;
   static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
-  static constexpr int kMinBlocks = MT == 1 ? 4 : 1;  // <= 128 registers (measured best; 5 spills into LDC)
+  static constexpr int kMinBlocks = MT == 1 ? 4 : (MT == 2 ? 3 : 2);  // register caps chosen by measurement
   static int span_hi(int L, int D) { return L - 1 + (D - 1); }  // p + 2K
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {

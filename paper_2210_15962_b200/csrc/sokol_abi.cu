@@ -91,9 +91,12 @@ constexpr uint32_t kSmemKeysMax = 32768;  // keys in smem up to 32 KB per walk
 
 struct Plan {
   sk::WalkParams P;
-  sk::SmemLayout lay;
-  bool keys_in_smem;
+  sk::SmemLayout lay_s;  // visited keys in shared memory
+  sk::SmemLayout lay_g;  // visited keys in an L2-resident global scratch
+  bool smem_keys_ok;
   int nw;
+  bool dry_run = false;  // compute the launch geometry only
+  int64_t resident = 0;  // walks resident at once (grid warps)
 };
 
 template <class Eval>
@@ -106,25 +109,42 @@ Plan make_plan(int L, int n) {
   pl.P.D = D;
   pl.P.K = D - 1;
   pl.P.cap = visited_capacity(n);
-  pl.keys_in_smem = pl.P.cap * 8u <= kSmemKeysMax;
-  pl.lay = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, pl.keys_in_smem, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                Eval::span_hi(L, D), Eval::kCeAliasKeys);
-  pl.P.warp_smem = pl.lay.total;
+  pl.smem_keys_ok = pl.P.cap * 8u <= kSmemKeysMax;
+  pl.lay_s = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, true, Eval::ext_bytes(L, D), Eval::kNeedsDl,
+                                  Eval::span_hi(L, D), Eval::kCeAliasKeys);
+  pl.lay_g = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, false, Eval::ext_bytes(L, D), Eval::kNeedsDl,
+                                  Eval::span_hi(L, D), Eval::kCeAliasKeys);
   return pl;
 }
 
+// Occupancy-driven placement of the visited keys: shared memory unless moving
+// them to L2 lets more walks be resident (measured: the L2 probes cost less
+// than the occupancy they buy once keys exceed ~8 KB per walk).
 template <int NW, bool TRACE, class Eval>
 int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   auto kern = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB>;
-  const size_t smem = size_t(pl.P.warp_smem) * kWPB;
-  SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  int sms = 0, per_sm = 0;
+  int sms = 0, per_s = 0, per_g = 0;
   SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem));
-  if (per_sm < 1) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM (smem " + std::to_string(smem) + ")");
+  const size_t smem_s = size_t(pl.lay_s.total) * kWPB, smem_g = size_t(pl.lay_g.total) * kWPB;
+  int max_optin = 0;
+  SK_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const bool s_ok = pl.smem_keys_ok && smem_s <= size_t(max_optin);
+  const bool g_ok = smem_g <= size_t(max_optin);
+  const size_t attr = std::max(s_ok ? smem_s : 0, g_ok ? smem_g : 0);
+  if (attr > 0) SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attr)));
+  if (s_ok) SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, kern, kWPB * 32, smem_s));
+  if (g_ok) SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_g, kern, kWPB * 32, smem_g));
+  const bool keys_in_smem = per_s >= per_g && per_s > 0;
+  const int per_sm = keys_in_smem ? per_s : per_g;
+  if (per_sm < 1) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM (smem " + std::to_string(smem_g) + ")");
+  const sk::SmemLayout lay = keys_in_smem ? pl.lay_s : pl.lay_g;
+  pl.P.warp_smem = lay.total;
+  const size_t smem = size_t(lay.total) * kWPB;
   const int64_t want = (pl.P.W + kWPB - 1) / kWPB;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms));
-  if (!pl.keys_in_smem) {
+  pl.resident = int64_t(per_sm) * sms * kWPB;
+  if (pl.dry_run) return SK_OK;
+  if (!keys_in_smem) {
     DevCache& c = cache_for(dev);
     int rc = grow(&c.gkeys, &c.gkeys_bytes, size_t(grid) * kWPB * pl.P.cap * 8u);
     if (rc) return rc;
@@ -132,7 +152,8 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   } else {
     pl.P.gkeys = nullptr;
   }
-  kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, pl.lay);
+  SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
   SK_CUDA(cudaGetLastError());
   return SK_OK;
 }
@@ -351,17 +372,15 @@ int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t* best_words, uint64_t
 
 int64_t sk_resident_walks(int L, int n) {
   if (validate(L, n, 1)) return -1;
-  int dev = 0, sms = 0, per_sm = 0;
+  int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  std::lock_guard<std::mutex> lk(g_mu);
   const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
   Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
-  const size_t smem = size_t(pl.P.warp_smem) * kWPB;
-  // the occupancy of the NW=1 instantiation is representative (same smem)
-  auto kern = sk::saw_walk_kernel<1, false, sk::EvalScalar, kWPB>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem) != cudaSuccess) return -1;
-  return int64_t(per_sm) * sms * kWPB;
+  pl.P.W = int64_t(1) << 40;
+  pl.dry_run = true;
+  const int rc = scalar ? launch_eval<false, sk::EvalScalar>(pl, 0, dev) : launch_fast<false>(pl, 0, dev);
+  return rc ? -1 : pl.resident;
 }
 
 int sk_shutdown(void) {
