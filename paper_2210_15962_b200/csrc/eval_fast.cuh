@@ -303,15 +303,11 @@ struct EvalFast {
       }
     }
     __syncwarp();
-    if (lane == 0) {
-      s[p] = int8_t(-sp);
-      __half* a = (p & 1) ? sp1 : sp0;
-      a[G.SPAD + (p >> 1)] = __int2half_rn(-sp);
-      if (!centre) {
-        s[q] = int8_t(-sq);
-        __half* b = (q & 1) ? sp1 : sp0;
-        b[G.SPAD + (q >> 1)] = __int2half_rn(-sq);
-      }
+    if (lane < (centre ? 1 : 2)) {  // lane 0 flips p, lane 1 flips q
+      const int x = lane ? q : p;
+      const int32_t sx = lane ? sq : sp;
+      s[x] = int8_t(-sx);
+      ((x & 1) ? sp1 : sp0)[G.SPAD + (x >> 1)] = __int2half_rn(-sx);
     }
     __syncwarp();
   }

@@ -50,18 +50,48 @@ __device__ __forceinline__ uint64_t key_of_words(const uint64_t (&w)[NW]) {  // 
   return h;
 }
 
-// Key of `w` with half index h flipped (bit D-1-h toggled), _kernels.py:250-253.
+// Visited-set identity.  The reference keys a pivot by key = mix64(u) with
+// u = h_{NW-1} ^ w_{NW-1}, h_0 = KEY_SEED, h_{i+1} = mix64(h_i ^ w_i)
+// (key_of_words, _kernels.py:46-53).  mix64 is a bijection on 64-bit words
+// (_kernels.py:32), so  key(x) == key(y)  <=>  u(x) == u(y): storing u instead
+// of the key gives the identical membership (including the reference's
+// cross-word collisions for D > 64) without the final mix64.  The prefixes
+// h_i of the current pivot are cached, so a candidate whose flipped bit lies
+// in word i costs (NW - 1 - i) mix64 calls -- zero for the last word.
 template <int NW>
-__device__ __forceinline__ uint64_t key_of_flipped(const uint64_t (&w)[NW], int D, int h) {
-  const int b = D - 1 - h;
-  uint64_t h64 = kKeySeed;
+struct KeyState {
+  uint64_t hp[NW];  // hp[i] = h_i of the current pivot
+
+  __device__ __forceinline__ void init(const uint64_t (&w)[NW]) {
+    hp[0] = kKeySeed;
 #pragma unroll
-  for (int i = 0; i < NW; i++) {
-    const uint64_t x = w[i] ^ ((b >> 6) == i ? (1ull << (b & 63)) : 0ull);
-    h64 = mix64(h64 ^ x);
+    for (int i = 0; i + 1 < NW; i++) hp[i + 1] = mix64(hp[i] ^ w[i]);
   }
-  return h64;
-}
+  __device__ __forceinline__ uint64_t u_of(const uint64_t (&w)[NW]) const { return hp[NW - 1] ^ w[NW - 1]; }
+
+  // u of the pivot with half index h flipped; chain[] receives the candidate's
+  // prefixes (valid from its flipped word on) for commit().
+  __device__ __forceinline__ uint64_t u_of_flip(const uint64_t (&w)[NW], int D, int h, uint64_t (&chain)[NW]) const {
+    const int b = D - 1 - h;
+    const int wi = b >> 6;
+    const uint64_t bit = 1ull << (b & 63);
+    uint64_t x = hp[0];
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+      if (i == wi) x = hp[i];  // prefix unchanged up to the flipped word
+      chain[i] = x;
+      if (i + 1 < NW && i >= wi) x = mix64(x ^ (w[i] ^ (i == wi ? bit : 0ull)));
+    }
+    return chain[NW - 1] ^ (w[NW - 1] ^ (wi == NW - 1 ? bit : 0ull));
+  }
+
+  __device__ __forceinline__ void commit(int D, int h, const uint64_t (&chain)[NW]) {
+    const int wi = (D - 1 - h) >> 6;
+#pragma unroll
+    for (int i = 1; i < NW; i++)
+      if (i > wi) hp[i] = chain[i];
+  }
+};
 
 template <int NW>
 __device__ __forceinline__ void toggle_half_bit(uint64_t (&w)[NW], int D, int h) {
@@ -87,18 +117,25 @@ __device__ __forceinline__ int32_t cand_delta(uint32_t key) { return (int32_t(ke
 // Occupancy lives in a bitmap so that key 0 is a legal key (no sentinel).
 // ---------------------------------------------------------------------------
 struct VisitedSet {
-  uint64_t* keys;  // [cap]
+  uint64_t* keys;  // [cap]  (stores u, see KeyState)
   uint32_t* occ;   // [cap/32] occupancy bits
   uint32_t mask;   // cap - 1, cap a power of two >= 32
+  uint32_t shift;  // 32 - log2(cap)
 
   __device__ __forceinline__ void clear(int lane) {
     for (uint32_t i = lane; i <= (mask >> 5); i += 32) occ[i] = 0u;
   }
 
-  // Warp-collective.  Returns true iff key present.  If absent and
-  // `insert_if_absent`, lane 0 writes it into the first free slot.
+  __device__ __forceinline__ static uint32_t home(uint64_t u, uint32_t shift) {
+    // Fibonacci hash of the folded identity (u itself is not uniformly mixed
+    // for D <= 64, where it is KEY_SEED ^ words)
+    return ((uint32_t(u) ^ uint32_t(u >> 32)) * 0x9E3779B1u) >> shift;
+  }
+
+  // Warp-collective.  Returns true iff u is present.  If absent and
+  // `insert_if_absent`, the lane at the first free slot writes it.
   __device__ __forceinline__ bool probe(uint64_t key, int lane, bool insert_if_absent) {
-    uint32_t start = uint32_t(key) & mask;
+    uint32_t start = home(key, shift);
     for (;;) {
       const uint32_t slot = (start + lane) & mask;
       const bool used = (occ[slot >> 5] >> (slot & 31)) & 1u;

@@ -137,10 +137,12 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   ev.init(P, sm, s, lane);
 
   // ---- visited set with P1 (_kernels.py:220-226) ------------------------
-  VisitedSet vs{sm.keys, sm.occ, P.cap - 1u};
+  VisitedSet vs{sm.keys, sm.occ, P.cap - 1u, uint32_t(__clz(P.cap) + 1)};
   vs.clear(lane);
   __syncwarp();
-  vs.probe(key_of_words<NW>(words), lane, true);
+  KeyState<NW> ks;
+  ks.init(words);
+  vs.probe(ks.u_of(words), lane, true);
 
   int32_t best_e = E;
   uint64_t best_w[NW];
@@ -173,10 +175,12 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
         ev.exclude(hc, lane);
         continue;
       }
-      const uint64_t nk = key_of_flipped<NW>(words, D, hc);
+      uint64_t chain[NW];
+      const uint64_t nk = ks.u_of_flip(words, D, hc, chain);
       if (!vs.probe(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
         hs = hc;
         dsel = cand_delta(m);
+        ks.commit(D, hc, chain);
         break;
       }
       ev.exclude(hc, lane);
