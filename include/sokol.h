@@ -78,6 +78,20 @@ int sk_saw_batch(int L, int n, const uint64_t *d_seeds, uint64_t master_seed, ui
                  int64_t *d_steps, uint8_t *d_dead, sk_batch_summary *d_summary, void *stream);
 
 /*
+ * R independent searches in one launch: the batch step
+ * of R concurrent solves, as run by runner.target_campaign
+ * (runner.py:294-317), whose repetitions the reference runs one after the
+ * other, each a full runner.solve batch loop (runner.py:213-291).
+ * Search r runs walkers [walker_begin, walker_begin + W) of batch
+ * d_batches[r] under master seed d_masters[r] (seeds derived on device
+ * exactly as sk_saw_batch with d_seeds == NULL) and writes d_summaries[r],
+ * which is therefore identical to the summary sk_saw_batch gives for that
+ * (master, batch, walker range).  Device arrays of R entries; asynchronous.
+ */
+int sk_saw_multi(int L, int n, const uint64_t *d_masters, const uint64_t *d_batches, int R,
+                 uint64_t walker_begin, int64_t W, sk_batch_summary *d_summaries, void *stream);
+
+/*
  * Traced batch: as sk_saw_batch plus the trajectory record of
  * _kernels.py:231-243, 267-270 (record=True), device memory:
  *   d_trace_words  [W][n+1][nw]  pivot after t moves (row 0 = first pivot)
@@ -114,6 +128,27 @@ int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t *best_words, uint64_t
  * current device (persistent grid size in warps).  Informational.
  */
 int64_t sk_resident_walks(int L, int n);
+
+/*
+ * Exhaustive Gray-code scan of the half-sequence space on the current device
+ * (SURVEY §8(f) row 2).  Replaces skewsaw._kernels.exhaustive_scan(length)
+ * (_kernels.py:290-323), called by saw.exhaustive_optimum (saw.py:151-168),
+ * whose single-threaded loop is capped at D <= 28 (saw.py:36); the device
+ * scan accepts D <= SK_MAX_EXHAUSTIVE_D.
+ *
+ * sk_exhaustive_scan: Gray indices g in [g_begin, g_begin + g_count) (the
+ *   half after reference step g is gray(g) = g ^ (g >> 1); g = 0 is the
+ *   all-plus start), asynchronous on `stream`.  Folds
+ *   key = (E << 44) | g into *d_min_key with an atomic min, so the caller
+ *   initialises it to UINT64_MAX and may split the space into any slices;
+ *   the final key's (E, g) is the reference's first minimum.
+ * sk_exhaustive_scan_host: the whole space, synchronous; returns exactly the
+ *   reference's (best_energy, best_bits), bit h of best_bits set iff half
+ *   spin h is -1.
+ */
+#define SK_MAX_EXHAUSTIVE_D 44
+int sk_exhaustive_scan(int L, uint64_t g_begin, uint64_t g_count, uint64_t *d_min_key, void *stream);
+int sk_exhaustive_scan_host(int L, int64_t *best_e_out, int64_t *best_bits_out);
 
 /* Release the library's cached device buffers (safe to call at any time). */
 int sk_shutdown(void);

@@ -70,6 +70,8 @@ def lib():
         L.so_saw_batch.restype = ctypes.c_int
         L.so_exhaustive_scan.argtypes = [ctypes.c_int, _i64p]
         L.so_exhaustive_scan.restype = ctypes.c_int64
+        L.so_exhaustive_range.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _u64p]
+        L.so_exhaustive_range.restype = ctypes.c_int64
         L.so_num_procs.argtypes = []
         L.so_num_procs.restype = ctypes.c_int
         _lib = L
@@ -187,6 +189,13 @@ def exhaustive_scan(length: int):
     bits = np.zeros(1, dtype=np.int64)
     e = int(lib().so_exhaustive_scan(length, _p(bits, _i64p)))
     return e, int(bits[0])
+
+
+def exhaustive_range(length: int, g_begin: int, g_count: int):
+    """(first-min energy, its Gray index g) over g in [g_begin, g_begin + g_count)."""
+    g = np.zeros(1, dtype=np.uint64)
+    e = int(lib().so_exhaustive_range(length, g_begin, g_count, _p(g, _u64p)))
+    return e, int(g[0])
 
 
 def solve_record(L, walkers, walk_factor=8, master_seed=1, max_nses=None, target_E=None, threads: int = 0):

@@ -341,3 +341,33 @@ int64_t so_exhaustive_scan(int L, int64_t *best_bits_out) {
     return best_e;
 }
 
+
+/*
+ * Slice of the same enumeration (test support for the device scan, which
+ * splits the Gray index range): the state entering index g_begin is the half
+ * gray(g_begin) (the reference's `bits` after step g_begin, _kernels.py:321),
+ * then steps g_begin+1 .. g_begin+g_count-1 run exactly as
+ * _kernels.py:313-322.  Returns the first minimum's energy and its index g.
+ */
+int64_t so_exhaustive_range(int L, uint64_t g_begin, uint64_t g_count, uint64_t *best_g_out) {
+    const int d = (L + 1) / 2;
+    int64_t *s = (int64_t *)malloc(sizeof(int64_t) * L);
+    int64_t *c = (int64_t *)calloc(L, sizeof(int64_t));
+    const uint64_t x = g_begin ^ (g_begin >> 1);
+    for (int h = 0; h < d; h++) s[h] = ((x >> h) & 1) ? -1 : 1;
+    expand_in_place(s, d);
+    int64_t e = init_sidelobes(s, c, L);
+    int64_t best_e = e;
+    uint64_t best_g = g_begin;
+    for (uint64_t g = g_begin + 1; g < g_begin + g_count; g++) {
+        uint64_t gg = g;
+        int h = 0;
+        while ((gg & 1) == 0) { gg >>= 1; h++; }
+        e += neighbor_delta(s, c, L, h);
+        apply_neighbor(s, c, L, h);
+        if (e < best_e) { best_e = e; best_g = g; }
+    }
+    free(s); free(c);
+    *best_g_out = best_g;
+    return best_e;
+}

@@ -20,7 +20,16 @@ from .runner import (
     target_campaign,
     throughput_report,
 )
-from .saw import WalkConfig, WalkResult, WalkTrace, key, run_walk, run_walk_traced
+from .saw import (
+    MAX_EXHAUSTIVE_D,
+    WalkConfig,
+    WalkResult,
+    WalkTrace,
+    exhaustive_optimum,
+    key,
+    run_walk,
+    run_walk_traced,
+)
 
 __version__ = "0.1.0"
 
@@ -28,5 +37,6 @@ __all__ = [
     "DecodeError", "decode", "encode", "EnergyRecord", "energy", "expand_skew", "half_dim",
     "merit_factor", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
     "derive_walk_seed", "solve", "target_campaign", "throughput_report", "WalkConfig",
-    "WalkResult", "WalkTrace", "key", "run_walk", "run_walk_traced",
+    "WalkResult", "WalkTrace", "key", "run_walk", "run_walk_traced", "MAX_EXHAUSTIVE_D",
+    "exhaustive_optimum",
 ]

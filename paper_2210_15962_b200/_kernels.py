@@ -9,6 +9,8 @@ reference's numba kernels, executed by libsokol.so on the current CUDA device:
         -> skewsaw._kernels.saw_walk    (_kernels.py:189-275)
     key_of_words(words)
         -> skewsaw._kernels.key_of_words (_kernels.py:46-53)
+    exhaustive_scan(length) -> (best_e, best_bits)
+        -> skewsaw._kernels.exhaustive_scan (_kernels.py:290-323)
 
 Unlike numba, the C ABI validates its arguments and raises ``SokolError``
 (a RuntimeError) on bad input or a CUDA failure.
@@ -85,3 +87,13 @@ def saw_walk(length, n, seed, best_words, trace_words, trace_deltas, record):
         be.ctypes.data, st.ctypes.data, dd.ctypes.data,
     ))
     return np.int64(be[0]), np.int64(st[0]), bool(dd[0])
+
+
+def exhaustive_scan(length):
+    """Minimum energy over all 2^D half sequences and the reference's argmin
+    (first minimum in Gray order); bit h of best_bits set iff half spin h is
+    -1.  Runs the device Gray-code scan (D <= SK_MAX_EXHAUSTIVE_D)."""
+    be = np.zeros(1, np.int64)
+    bb = np.zeros(1, np.int64)
+    _lib.check(_lib.load().sk_exhaustive_scan_host(int(length), be.ctypes.data, bb.ctypes.data))
+    return np.int64(be[0]), np.int64(bb[0])

@@ -22,6 +22,7 @@ SK_ERR_CUDA = -3
 SK_ERR_NOMEM = -4
 SK_MAX_L = 1023
 SK_MAX_WORDS = 8
+SK_MAX_EXHAUSTIVE_D = 44
 
 VARIANT_AUTO = 0
 VARIANT_SCALAR = 1
@@ -36,10 +37,13 @@ EXPORTS = (
     "sk_set_variant",
     "sk_get_variant",
     "sk_saw_batch",
+    "sk_saw_multi",
     "sk_saw_trace",
     "sk_saw_batch_host",
     "sk_saw_walk_host",
     "sk_resident_walks",
+    "sk_exhaustive_scan",
+    "sk_exhaustive_scan_host",
     "sk_shutdown",
 )
 
@@ -83,6 +87,8 @@ def _declare(lib):
     lib.sk_get_variant.restype = _i
     lib.sk_saw_batch.argtypes = [_i, _i, _vp, _u64, _u64, _u64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
     lib.sk_saw_batch.restype = _i
+    lib.sk_saw_multi.argtypes = [_i, _i, _vp, _vp, _i, _u64, _i64, _vp, _vp]
+    lib.sk_saw_multi.restype = _i
     lib.sk_saw_trace.argtypes = [_i, _i, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     lib.sk_saw_trace.restype = _i
     lib.sk_saw_batch_host.argtypes = [_i, _i, _vp, _i64, _vp, _vp, _vp, _vp]
@@ -91,6 +97,10 @@ def _declare(lib):
     lib.sk_saw_walk_host.restype = _i
     lib.sk_resident_walks.argtypes = [_i, _i]
     lib.sk_resident_walks.restype = _i64
+    lib.sk_exhaustive_scan.argtypes = [_i, _u64, _u64, _vp, _vp]
+    lib.sk_exhaustive_scan.restype = _i
+    lib.sk_exhaustive_scan_host.argtypes = [_i, _vp, _vp]
+    lib.sk_exhaustive_scan_host.restype = _i
     lib.sk_shutdown.restype = _i
 
 

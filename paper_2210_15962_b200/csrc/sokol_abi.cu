@@ -17,6 +17,7 @@
 #include "../../include/sokol.h"
 #include "eval_scalar.cuh"
 #include "eval_fast.cuh"
+#include "exhaustive.cuh"
 #include "walk_engine.cuh"
 
 namespace {
@@ -205,14 +206,22 @@ int launch_fast(Plan& pl, cudaStream_t st, int dev) {
   return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
 }
 
+// R > 0 with masters/batches: multi-search mode, W walks per search
 template <bool TRACE>
 int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, uint64_t walker_begin, int64_t W,
         int64_t* best_e, uint64_t* best_words, int64_t* steps, uint8_t* dead, sk_batch_summary* summary,
-        uint64_t* trace_words, int64_t* trace_deltas, cudaStream_t st) {
+        uint64_t* trace_words, int64_t* trace_deltas, cudaStream_t st, const uint64_t* masters = nullptr,
+        const uint64_t* batches = nullptr, int R = 1) {
   int rc = validate(L, n, W);
   if (rc) return rc;
   if (summary && walker_begin + uint64_t(W) > (uint64_t(1) << 32))
     return fail(SK_ERR_ARG, "walker_begin + W must be < 2^32 when a summary is requested");
+  const int64_t W_rep = W;
+  if (masters) {
+    if (R < 1) return fail(SK_ERR_ARG, "search count must be >= 1");
+    if (W > (int64_t(1) << 40) / R) return fail(SK_ERR_ARG, "R * W too large");
+    W = W_rep * R;
+  }
   std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
   SK_CUDA(cudaGetDevice(&dev));
@@ -230,6 +239,9 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
   pl.P.trace_words = trace_words;
   pl.P.trace_deltas = trace_deltas;
   pl.P.best_words = best_words;
+  pl.P.masters = masters;
+  pl.P.batches = batches;
+  pl.P.W_rep = W_rep;
   if (summary && !best_words && W > 0) {
     DevCache& c = cache_for(dev);
     rc = grow(&c.words, &c.words_bytes, size_t(W) * pl.nw * 8u);
@@ -237,7 +249,7 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
     pl.P.best_words = static_cast<uint64_t*>(c.words);
   }
   if (summary) {
-    sk::summary_init_kernel<<<1, 32, 0, st>>>(summary);
+    sk::summary_init_kernel<<<masters ? R : 1, 32, 0, st>>>(summary);
     SK_CUDA(cudaGetLastError());
   }
   if (W > 0) {
@@ -245,11 +257,50 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
     if (rc) return rc;
   }
   if (summary && W > 0) {
-    sk::summary_finish_kernel<<<1, 32, 0, st>>>(summary, pl.P.best_words, pl.nw, walker_begin);
+    sk::summary_finish_kernel<<<masters ? R : 1, 32, 0, st>>>(summary, pl.P.best_words, pl.nw, walker_begin, W_rep);
     SK_CUDA(cudaGetLastError());
   }
   return SK_OK;
 }
+
+// ---- exhaustive scan (exhaustive.cuh) ---------------------------------------
+int exh_validate(int L) {
+  if (L < 3 || (L % 2) == 0) return fail(SK_ERR_ARG, "length must be odd and >= 3, got " + std::to_string(L));
+  if ((L + 1) / 2 > SK_MAX_EXHAUSTIVE_D)
+    return fail(SK_ERR_UNSUPPORTED, "L=" + std::to_string(L) + " has D=" + std::to_string((L + 1) / 2) +
+                                        " free components; the device scan is capped at D=" +
+                                        std::to_string(SK_MAX_EXHAUSTIVE_D));
+  return SK_OK;
+}
+
+// chunk of consecutive Gray indices per thread: long enough to amortise the
+// O(L^2) state rebuild, short enough to give every SM work
+int exh_chunk_log2(int D) { return std::max(4, std::min(16, D - 19)); }
+
+template <int KMAX>
+int exh_launch(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key, cudaStream_t st, int dev) {
+  auto kern = sk::exhaustive_kernel<KMAX>;
+  const int cl2 = exh_chunk_log2((L + 1) / 2);
+  const uint64_t nchunks = ((g_end - g_begin) + (1ull << cl2) - 1) >> cl2;
+  int sms = 0, per = 0;
+  SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0));
+  const uint64_t want = (nchunks + 255) / 256;
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per, 1)) * sms));
+  kern<<<unsigned(grid), 256, 0, st>>>(L, g_begin, g_end, cl2, key);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int exh_run(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key, cudaStream_t st, int dev) {
+  const int K = (L + 1) / 2 - 1;
+  if (K <= 15) return exh_launch<15>(L, g_begin, g_end, key, st, dev);
+  if (K <= 23) return exh_launch<23>(L, g_begin, g_end, key, st, dev);
+  if (K <= 31) return exh_launch<31>(L, g_begin, g_end, key, st, dev);
+  return exh_launch<43>(L, g_begin, g_end, key, st, dev);
+}
+
+__global__ void exh_key_init(unsigned long long* k) { *k = ~0ull; }
 
 }  // namespace
 
@@ -272,6 +323,14 @@ int sk_saw_batch(int L, int n, const uint64_t* d_seeds, uint64_t master_seed, ui
                  sk_batch_summary* d_summary, void* stream) {
   return run<false>(L, n, d_seeds, master_seed, batch, walker_begin, W, d_best_e, d_best_words, d_steps, d_dead,
                     d_summary, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int sk_saw_multi(int L, int n, const uint64_t* d_masters, const uint64_t* d_batches, int R, uint64_t walker_begin,
+                 int64_t W, sk_batch_summary* d_summaries, void* stream) {
+  if (!d_masters || !d_batches || !d_summaries) return fail(SK_ERR_ARG, "sk_saw_multi needs masters, batches, summaries");
+  if (R < 1) return fail(SK_ERR_ARG, "search count R must be >= 1");
+  return run<false>(L, n, nullptr, 0, 0, walker_begin, W, nullptr, nullptr, nullptr, nullptr, d_summaries, nullptr,
+                    nullptr, static_cast<cudaStream_t>(stream), d_masters, d_batches, R);
 }
 
 int sk_saw_trace(int L, int n, const uint64_t* d_seeds, int64_t W, int64_t* d_best_e, uint64_t* d_best_words,
@@ -381,6 +440,45 @@ int64_t sk_resident_walks(int L, int n) {
   pl.dry_run = true;
   const int rc = scalar ? launch_eval<false, sk::EvalScalar>(pl, 0, dev) : launch_fast<false>(pl, 0, dev);
   return rc ? -1 : pl.resident;
+}
+
+int sk_exhaustive_scan(int L, uint64_t g_begin, uint64_t g_count, uint64_t* d_min_key, void* stream) {
+  int rc = exh_validate(L);
+  if (rc) return rc;
+  if (!d_min_key) return fail(SK_ERR_ARG, "sk_exhaustive_scan: null key");
+  const int D = (L + 1) / 2;
+  const uint64_t total = 1ull << D;
+  if (g_begin > total || g_count > total - g_begin)
+    return fail(SK_ERR_ARG, "Gray index range exceeds 2^D");
+  if (g_count == 0) return SK_OK;
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  return exh_run(L, g_begin, g_begin + g_count, reinterpret_cast<unsigned long long*>(d_min_key),
+                 static_cast<cudaStream_t>(stream), dev);
+}
+
+int sk_exhaustive_scan_host(int L, int64_t* best_e_out, int64_t* best_bits_out) {
+  int rc = exh_validate(L);
+  if (rc) return rc;
+  if (!best_e_out || !best_bits_out) return fail(SK_ERR_ARG, "sk_exhaustive_scan_host: null output");
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  unsigned long long* dkey = nullptr;
+  SK_CUDA(cudaMalloc(&dkey, 8));
+  cudaStream_t st = 0;
+  exh_key_init<<<1, 1, 0, st>>>(dkey);
+  const int D = (L + 1) / 2;
+  const uint64_t total = 1ull << D, slice = 1ull << 36;  // bounded launches (~1 s each at D = 44)
+  for (uint64_t b = 0; b < total && rc == SK_OK; b += slice) rc = exh_run(L, b, std::min(total, b + slice), dkey, st, dev);
+  unsigned long long key = 0;
+  if (rc == SK_OK && cudaMemcpy(&key, dkey, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(SK_ERR_CUDA, std::string("sk_exhaustive_scan_host: ") + cudaGetErrorString(cudaGetLastError()));
+  cudaFree(dkey);
+  if (rc) return rc;
+  const uint64_t g = key & ((1ull << sk::kExhKeyShift) - 1);
+  *best_e_out = int64_t(key >> sk::kExhKeyShift);
+  *best_bits_out = int64_t(g ^ (g >> 1));
+  return SK_OK;
 }
 
 int sk_shutdown(void) {

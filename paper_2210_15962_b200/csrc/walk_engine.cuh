@@ -32,6 +32,12 @@ struct WalkParams {
   uint64_t* trace_words;    // TRACE only: [W][n+1][nw]
   int64_t* trace_deltas;    // TRACE only: [W][n][D]
   uint64_t* gkeys;          // global visited keys [nwarps][cap] or null (keys in smem)
+  // multi-search mode (sk_saw_multi): W = R * W_rep walks; walk w belongs to
+  // search r = w / W_rep with its own master seed and batch index, and
+  // reduces into summary[r].  masters == nullptr: a single search.
+  const uint64_t* masters;
+  const uint64_t* batches;
+  int64_t W_rep;
   uint32_t warp_smem;       // bytes of dynamic smem per warp
 };
 
@@ -100,7 +106,17 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-(L-1), span_hi], zero outside [0, L)
 
   // ---- first pivot (_kernels.py:201-209) --------------------------------
-  const uint64_t seed = P.seeds ? P.seeds[w] : derive_walk_seed(P.master, P.batch, P.walker_begin + uint64_t(w));
+  uint64_t master = P.master, batch = P.batch;
+  int64_t wi = w;  // walker index within its search (before walker_begin)
+  sk_batch_summary* summary = P.summary;
+  if (P.masters) {
+    const int64_t r = w / P.W_rep;
+    wi = w - r * P.W_rep;
+    master = P.masters[r];
+    batch = P.batches[r];
+    summary += r;
+  }
+  const uint64_t seed = P.seeds ? P.seeds[w] : derive_walk_seed(master, batch, P.walker_begin + uint64_t(wi));
   for (int i = lane; i < int(lay.span); i += 32) sm.s8[i] = 0;
   __syncwarp();
   for (int h = lane; h < D; h += 32) {
@@ -215,10 +231,10 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
     if (P.best_e) P.best_e[w] = best_e;
     if (P.steps_out) P.steps_out[w] = steps;
     if (P.dead_out) P.dead_out[w] = dead ? 1 : 0;
-    if (P.summary) {
-      const uint64_t key = (uint64_t(uint32_t(best_e)) << 32) | uint64_t(uint32_t(P.walker_begin + uint64_t(w)));
-      atomicMin(reinterpret_cast<unsigned long long*>(&P.summary->min_key), (unsigned long long)key);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.summary->steps_sum), (unsigned long long)steps);
+    if (summary) {
+      const uint64_t key = (uint64_t(uint32_t(best_e)) << 32) | uint64_t(uint32_t(P.walker_begin + uint64_t(wi)));
+      atomicMin(reinterpret_cast<unsigned long long*>(&summary->min_key), (unsigned long long)key);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&summary->steps_sum), (unsigned long long)steps);
     }
   }
   if (P.best_words && lane < nw_rt) {
@@ -242,8 +258,10 @@ __global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(Wa
   for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval>(P, lay, wbase, gkeys, w, lane);
 }
 
-// Summary init / finish (tiny single-warp kernels on the same stream).
+// Summary init / finish (tiny kernels on the same stream), one block per
+// search: summary r covers walks [r * W_rep, (r + 1) * W_rep).
 __global__ void summary_init_kernel(sk_batch_summary* s) {
+  s += blockIdx.x;
   if (threadIdx.x == 0) {
     s->min_key = ~0ull;
     s->steps_sum = 0;
@@ -252,10 +270,11 @@ __global__ void summary_init_kernel(sk_batch_summary* s) {
 }
 
 __global__ void summary_finish_kernel(sk_batch_summary* s, const uint64_t* best_words, int nw,
-                                      uint64_t walker_begin) {
+                                      uint64_t walker_begin, int64_t W_rep) {
+  s += blockIdx.x;
   const uint64_t key = s->min_key;
   if (key == ~0ull) return;
-  const uint64_t local = uint64_t(uint32_t(key)) - uint32_t(walker_begin);
+  const uint64_t local = uint64_t(blockIdx.x) * uint64_t(W_rep) + (uint64_t(uint32_t(key)) - uint32_t(walker_begin));
   if (threadIdx.x < nw) s->best_words[threadIdx.x] = best_words[local * nw + threadIdx.x];
 }
 

@@ -78,6 +78,30 @@ def merge_across_ranks(win: BatchResult | None, steps: int, nw: int, process_gro
     return BatchResult(gkey >> 32, gkey & 0xFFFFFFFF, int(pv[0]), pv[1:].view(np.uint64).copy())
 
 
+def merge_many_across_ranks(wins, steps, nw: int, process_group, device):
+    """merge_across_ranks for R searches at once: one all-reduce MIN over R
+    keys and one all-reduce SUM over R x (1 + nw) payload words."""
+    import torch
+    import torch.distributed as dist
+
+    R = len(wins)
+    big = (1 << 63) - 1
+    keys = np.array([((w.best_E << 32) | w.walker) if w is not None else big for w in wins], dtype=np.int64)
+    kt = torch.from_numpy(keys.copy()).to(device)
+    dist.all_reduce(kt, op=dist.ReduceOp.MIN, group=process_group)
+    gkeys = kt.cpu().numpy()
+    payload = np.zeros((R, 1 + nw), dtype=np.int64)
+    payload[:, 0] = steps
+    for r, w in enumerate(wins):
+        if w is not None and int(keys[r]) == int(gkeys[r]):
+            payload[r, 1:] = np.asarray(w.best_words, dtype=np.uint64).view(np.int64)
+    pt = torch.from_numpy(payload).to(device)
+    dist.all_reduce(pt, op=dist.ReduceOp.SUM, group=process_group)
+    pv = pt.cpu().numpy()
+    return [BatchResult(int(g) >> 32, int(g) & 0xFFFFFFFF, int(pv[r, 0]), pv[r, 1:].view(np.uint64).copy())
+            for r, g in enumerate(gkeys)]
+
+
 class BatchEngine:
     """Runs batches of W walks of length n = walk_factor * D on GPU(s)."""
 
@@ -156,3 +180,46 @@ class BatchEngine:
     def run_batch(self, batch: int) -> BatchResult:
         self.launch(batch)
         return self.collect()
+
+    # ---- R concurrent searches (sk_saw_multi) --------------------------------
+    def run_multi(self, masters, batches) -> list[BatchResult]:
+        """One batch of each of R independent searches (same L, W, n; own
+        master seed and batch index) in one launch per device.  Result r is
+        identical to BatchEngine(L, W, n, masters[r]).run_batch(batches[r])."""
+        torch = self.torch
+        R = len(masters)
+        if R != len(batches) or R < 1:
+            raise ValueError("masters and batches must be non-empty and of equal length")
+        mb = np.empty((2, R), dtype=np.uint64)
+        mb[0] = [int(m) & ((1 << 64) - 1) for m in masters]
+        mb[1] = [int(b) for b in batches]
+        host_in = torch.from_numpy(mb.view(np.int64)).pin_memory()
+        outs = []
+        for i, (dev, begin, cnt) in enumerate(self.parts):
+            with torch.cuda.device(dev):
+                st = self.streams[i]
+                with torch.cuda.stream(st):
+                    d_in = host_in.to(torch.device("cuda", dev), non_blocking=True)
+                    summ = torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, device=dev)
+                _lib.check(self.lib.sk_saw_multi(
+                    self.L, self.n, d_in[0].data_ptr(), d_in[1].data_ptr(), R, int(begin), int(cnt),
+                    summ.data_ptr(), st.cuda_stream,
+                ))
+                with torch.cuda.stream(st):
+                    h = torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)
+                    h.copy_(summ, non_blocking=True)
+                outs.append((h, d_in, summ))
+        for st in self.streams:
+            st.synchronize()
+        wins, steps = [], []
+        for r in range(R):
+            local = [x for x in (decode_summary(o[0][r].numpy().view(np.uint64), self.nw) for o in outs) if x is not None]
+            steps.append(sum(x.steps_sum for x in local))
+            wins.append(min(local, key=lambda x: (x.best_E, x.walker)) if local else None)
+        if self.pg is None:
+            return [BatchResult(w.best_E, w.walker, s, w.best_words) for w, s in zip(wins, steps)]
+        import torch.distributed as dist
+
+        dev = self.parts[0][0]
+        tdev = torch.device("cuda", dev) if dist.get_backend(self.pg) == "nccl" else torch.device("cpu")
+        return merge_many_across_ranks(wins, steps, self.nw, self.pg, tdev)

@@ -117,3 +117,16 @@ def test_dead_end_tiny_space(oracle, L, seed):
     # test_saw.py:111-116: L=3 walk dies after 3 steps with best E = 1
     be, st, dead, *_ = oracle.saw_walk(L, 8 * 2, seed)
     assert (be, st, dead) == (1, 3, True)
+
+
+def test_exhaustive_range_slices_compose(oracle):
+    # the slice scan used as the device checker composes to the full scan
+    for L in (9, 21, 27):
+        D = (L + 1) // 2
+        total = 1 << D
+        e_all, bits = oracle.exhaustive_scan(L)
+        cuts = [0, 1, total // 3, total // 2 + 5, total]
+        parts = [oracle.exhaustive_range(L, a, b - a) for a, b in zip(cuts, cuts[1:])]
+        e, g = min(parts)
+        assert e == e_all and g ^ (g >> 1) == bits
+        assert oracle.exhaustive_range(L, 0, total) == (e, g)
