@@ -150,6 +150,25 @@ int64_t sk_resident_walks(int L, int n);
 int sk_exhaustive_scan(int L, uint64_t g_begin, uint64_t g_count, uint64_t *d_min_key, void *stream);
 int sk_exhaustive_scan_host(int L, int64_t *best_e_out, int64_t *best_bits_out);
 
+/*
+ * Batched neighbourhood evaluation and moves, S
+ * independent states in the reference's own array layout, device memory,
+ * asynchronous on `stream`:
+ *   d_s [S][L] int64 full +-1 sequence,  d_c [S][L] int64, d_c[k] = C_k,
+ *   d_deltas [S][D] int64,  d_h [S] int64 half index in [0, D).
+ * sk_all_neighbor_deltas replaces skewsaw._kernels.all_neighbor_deltas(s, c,
+ *   out) (_kernels.py:162-165 over neighbor_delta, 85-123), called by
+ *   neighborhood.compute_deltas (neighborhood.py:80-90).
+ * sk_apply_neighbor replaces skewsaw._kernels.apply_neighbor(s, c, h)
+ *   (_kernels.py:126-158), called by neighborhood.apply_flip
+ *   (neighborhood.py:93-100); a state whose h is out of range is left
+ *   unchanged (the Python layer raises before calling, as the reference does).
+ * Same int64 four-product arithmetic as the reference, for any +-1 input.
+ */
+int sk_all_neighbor_deltas(int L, int64_t S, const int64_t *d_s, const int64_t *d_c, int64_t *d_deltas,
+                           void *stream);
+int sk_apply_neighbor(int L, int64_t S, int64_t *d_s, int64_t *d_c, const int64_t *d_h, void *stream);
+
 /* Release the library's cached device buffers (safe to call at any time). */
 int sk_shutdown(void);
 

@@ -133,6 +133,11 @@ def all_neighbor_deltas(length: int, s, c) -> np.ndarray:
     return out
 
 
+def apply_neighbor(length: int, s, c, h: int):
+    """In place on int64 arrays (_kernels.py:126-158)."""
+    lib().so_apply_neighbor(length, _p(s, _i64p), _p(c, _i64p), int(h))
+
+
 def saw_walk(length: int, n: int, seed: int, record: bool = False):
     """Returns (best_e, steps, dead, best_words, trace_words|None, trace_deltas|None)."""
     d = (length + 1) // 2

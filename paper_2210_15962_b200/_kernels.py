@@ -97,3 +97,46 @@ def exhaustive_scan(length):
     bb = np.zeros(1, np.int64)
     _lib.check(_lib.load().sk_exhaustive_scan_host(int(length), be.ctypes.data, bb.ctypes.data))
     return np.int64(be[0]), np.int64(bb[0])
+
+
+def _device_copy(arr):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+
+
+def all_neighbor_deltas(s, c, out):
+    """out[h] = neighbor_delta(s, c, h) for every half index h
+    (_kernels.py:162-165); `s`, `c` int64[L] (c[k] = C_k), `out` int64[D].
+    Also accepts stacked states: s, c int64[S, L], out int64[S, D]."""
+    import torch
+
+    s = np.asarray(s)
+    L = int(s.shape[-1])
+    S = int(np.prod(s.shape[:-1], dtype=np.int64)) if s.ndim > 1 else 1
+    _req(out, np.int64, "out", s.shape[:-1] + ((L + 1) // 2,))
+    ds, dc = _device_copy(s.astype(np.int64, copy=False)), _device_copy(np.asarray(c, dtype=np.int64))
+    dout = torch.empty(out.shape, dtype=torch.int64, device=ds.device)
+    _lib.check(_lib.load().sk_all_neighbor_deltas(L, S, ds.data_ptr(), dc.data_ptr(), dout.data_ptr(),
+                                                  torch.cuda.current_stream().cuda_stream))
+    out[...] = dout.cpu().numpy()
+
+
+def apply_neighbor(s, c, h):
+    """Move to neighbour h in place (_kernels.py:126-158): even-lag sidelobes
+    of `c` updated, spins p = h and q = L-1-h of `s` negated.  Stacked
+    states (s, c int64[S, L]) take h as an int64[S] array."""
+    import torch
+
+    _req(s, np.int64, "s")
+    _req(c, np.int64, "c", s.shape)
+    L = int(s.shape[-1])
+    S = int(np.prod(s.shape[:-1], dtype=np.int64)) if s.ndim > 1 else 1
+    hv = np.asarray(h, dtype=np.int64).reshape(S)
+    if np.any((hv < 0) | (hv >= (L + 1) // 2)):
+        raise ValueError(f"flip index out of range for D={(L + 1) // 2}")
+    ds, dc, dh = _device_copy(s), _device_copy(c), _device_copy(hv)
+    _lib.check(_lib.load().sk_apply_neighbor(L, S, ds.data_ptr(), dc.data_ptr(), dh.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+    s[...] = ds.cpu().numpy()
+    c[...] = dc.cpu().numpy()

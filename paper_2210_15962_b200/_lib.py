@@ -44,6 +44,8 @@ EXPORTS = (
     "sk_resident_walks",
     "sk_exhaustive_scan",
     "sk_exhaustive_scan_host",
+    "sk_all_neighbor_deltas",
+    "sk_apply_neighbor",
     "sk_shutdown",
 )
 
@@ -101,6 +103,10 @@ def _declare(lib):
     lib.sk_exhaustive_scan.restype = _i
     lib.sk_exhaustive_scan_host.argtypes = [_i, _vp, _vp]
     lib.sk_exhaustive_scan_host.restype = _i
+    lib.sk_all_neighbor_deltas.argtypes = [_i, _i64, _vp, _vp, _vp, _vp]
+    lib.sk_all_neighbor_deltas.restype = _i
+    lib.sk_apply_neighbor.argtypes = [_i, _i64, _vp, _vp, _vp, _vp]
+    lib.sk_apply_neighbor.restype = _i
     lib.sk_shutdown.restype = _i
 
 

@@ -18,6 +18,7 @@
 #include "eval_scalar.cuh"
 #include "eval_fast.cuh"
 #include "exhaustive.cuh"
+#include "neighborhood.cuh"
 #include "walk_engine.cuh"
 
 namespace {
@@ -478,6 +479,41 @@ int sk_exhaustive_scan_host(int L, int64_t* best_e_out, int64_t* best_bits_out) 
   const uint64_t g = key & ((1ull << sk::kExhKeyShift) - 1);
   *best_e_out = int64_t(key >> sk::kExhKeyShift);
   *best_bits_out = int64_t(g ^ (g >> 1));
+  return SK_OK;
+}
+
+// ---- batched neighbourhood (neighborhood.cuh) --------------------------------
+static int nb_grid(int64_t S, int dev, int* grid) {
+  int sms = 0;
+  SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t want = (S + 7) / 8;  // 8 warps (states) per 256-thread block
+  *grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
+  return SK_OK;
+}
+
+int sk_all_neighbor_deltas(int L, int64_t S, const int64_t* d_s, const int64_t* d_c, int64_t* d_deltas, void* stream) {
+  int rc = validate(L, 1, S);
+  if (rc) return rc;
+  if (S == 0) return SK_OK;
+  if (!d_s || !d_c || !d_deltas) return fail(SK_ERR_ARG, "sk_all_neighbor_deltas: null buffer");
+  int dev = 0, grid = 1;
+  SK_CUDA(cudaGetDevice(&dev));
+  if ((rc = nb_grid(S, dev, &grid))) return rc;
+  sk::neighbor_deltas_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(L, S, d_s, d_c, d_deltas);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int sk_apply_neighbor(int L, int64_t S, int64_t* d_s, int64_t* d_c, const int64_t* d_h, void* stream) {
+  int rc = validate(L, 1, S);
+  if (rc) return rc;
+  if (S == 0) return SK_OK;
+  if (!d_s || !d_c || !d_h) return fail(SK_ERR_ARG, "sk_apply_neighbor: null buffer");
+  int dev = 0, grid = 1;
+  SK_CUDA(cudaGetDevice(&dev));
+  if ((rc = nb_grid(S, dev, &grid))) return rc;
+  sk::apply_neighbor_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(L, S, d_s, d_c, d_h);
+  SK_CUDA(cudaGetLastError());
   return SK_OK;
 }
 
