@@ -266,9 +266,14 @@ struct EvalFast {
     const bool centre = (p == q);
     const int32_t sp = s[p];
     const int32_t sq = s[q];
-    const int kx = centre ? -1 : q - p;  // the lag whose p+k term is excluded
     const int csh = centre ? 1 : 0;      // centre: s_{p+k} = s_{p-k}, so v = (sum) / 2
     const int32_t sp4 = 4 * sp;
+    // The lag k = q - p excludes its s_{p+k} = s_q term: s_q is zeroed for the
+    // duration of the update (it is overwritten with -s_q below), so every
+    // lane loads s_{p+k} unconditionally.
+    __syncwarp();
+    if (lane == 0 && !centre) s[q] = 0;
+    __syncwarp();
     // C_k -= 4 v_k(h*) for every even lag (apply_neighbor, _kernels.py:126-158);
     // lags with v_k = 0 leave C_k and its copies untouched
 #pragma unroll
@@ -276,7 +281,7 @@ struct EvalFast {
       const int j = 1 + lane + 32 * r;
       const int k = 2 * min(j, K);  // clamped so idle lanes read inside the padded span
       const int32_t a = s[p - k];
-      const int32_t b = (k == kx) ? 0 : int32_t(s[p + k]);
+      const int32_t b = s[p + k];
       const int32_t v = (a + b) >> csh;
       if (v != 0 && j <= K) {
         ce[r] -= sp4 * v;

@@ -78,7 +78,7 @@ struct KeyState {
     uint64_t x = hp[0];
 #pragma unroll
     for (int i = 0; i < NW; i++) {
-      if (i == wi) x = hp[i];  // prefix unchanged up to the flipped word
+      x = (i == wi) ? hp[i] : x;  // prefix unchanged up to the flipped word (selects: no local memory)
       chain[i] = x;
       if (i + 1 < NW && i >= wi) x = mix64(x ^ (w[i] ^ (i == wi ? bit : 0ull)));
     }
@@ -88,17 +88,17 @@ struct KeyState {
   __device__ __forceinline__ void commit(int D, int h, const uint64_t (&chain)[NW]) {
     const int wi = (D - 1 - h) >> 6;
 #pragma unroll
-    for (int i = 1; i < NW; i++)
-      if (i > wi) hp[i] = chain[i];
+    for (int i = 1; i < NW; i++) hp[i] = (i > wi) ? chain[i] : hp[i];
   }
 };
 
 template <int NW>
 __device__ __forceinline__ void toggle_half_bit(uint64_t (&w)[NW], int D, int h) {
   const int b = D - 1 - h;
+  const uint64_t bit = 1ull << (b & 63);
+  // selects, not a conditional store: a data-dependent index would push w[] to local memory
 #pragma unroll
-  for (int i = 0; i < NW; i++)
-    if ((b >> 6) == i) w[i] ^= 1ull << (b & 63);
+  for (int i = 0; i < NW; i++) w[i] ^= ((b >> 6) == i) ? bit : 0ull;
 }
 
 __device__ __forceinline__ uint32_t pack_cand(int32_t delta, int h) {
@@ -121,6 +121,19 @@ struct VisitedSet {
   uint32_t* occ;   // [cap/32] occupancy bits
   uint32_t mask;   // cap - 1, cap a power of two >= 32
   uint32_t shift;  // 32 - log2(cap)
+  uint32_t keys_s = 0;  // shared-window address of keys when they live in shared memory, else 0
+
+  __device__ __forceinline__ void bind_shared() {
+    keys_s = __isShared(keys) ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
+  }
+  __device__ __forceinline__ uint64_t load_key(uint32_t slot) const {
+    if (keys_s) {  // explicit LDS: generic loads of shared data cost extra latency on the probe path
+      uint64_t v;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(keys_s + slot * 8u));
+      return v;
+    }
+    return keys[slot];
+  }
 
   __device__ __forceinline__ void clear(int lane) {
     for (uint32_t i = lane; i <= (mask >> 5); i += 32) occ[i] = 0u;
@@ -142,13 +155,16 @@ struct VisitedSet {
       const uint32_t empty_mask = __ballot_sync(kFull, !used);
       // lanes strictly before the first empty slot are the live probe run
       const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
-      const bool hit = ((run >> lane) & 1u) && keys[slot] == key;
+      const bool hit = ((run >> lane) & 1u) && load_key(slot) == key;
       if (__any_sync(kFull, hit)) return true;
       if (empty_mask) {
         if (insert_if_absent) {
           const int first = __ffs(empty_mask) - 1;
           if (lane == first) {
-            keys[slot] = key;
+            if (keys_s)
+              asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys_s + slot * 8u), "l"(key) : "memory");
+            else
+              keys[slot] = key;
             atomicOr(&occ[slot >> 5], 1u << (slot & 31));
           }
           __syncwarp();

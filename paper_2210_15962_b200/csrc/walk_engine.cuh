@@ -154,6 +154,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
 
   // ---- visited set with P1 (_kernels.py:220-226) ------------------------
   VisitedSet vs{sm.keys, sm.occ, P.cap - 1u, uint32_t(__clz(P.cap) + 1)};
+  vs.bind_shared();
   vs.clear(lane);
   __syncwarp();
   KeyState<NW> ks;
