@@ -190,25 +190,34 @@ class BatchEngine:
         R = len(masters)
         if R != len(batches) or R < 1:
             raise ValueError("masters and batches must be non-empty and of equal length")
-        mb = np.empty((2, R), dtype=np.uint64)
+        cache = self.__dict__.setdefault("_multi_cache", {})  # pinned/device buffers per search count
+        if R not in cache:
+            host_in = torch.empty((2, R), dtype=torch.int64, pin_memory=True)
+            per_dev = []
+            for dev, _, _ in self.parts:
+                with torch.cuda.device(dev):
+                    per_dev.append((torch.empty((2, R), dtype=torch.int64, device=dev),
+                                    torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, device=dev),
+                                    torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)))
+            cache[R] = (host_in, per_dev)
+        host_in, per_dev = cache[R]
+        mb = host_in.numpy().view(np.uint64)
         mb[0] = [int(m) & ((1 << 64) - 1) for m in masters]
         mb[1] = [int(b) for b in batches]
-        host_in = torch.from_numpy(mb.view(np.int64)).pin_memory()
         outs = []
         for i, (dev, begin, cnt) in enumerate(self.parts):
+            d_in, summ, h = per_dev[i]
             with torch.cuda.device(dev):
                 st = self.streams[i]
                 with torch.cuda.stream(st):
-                    d_in = host_in.to(torch.device("cuda", dev), non_blocking=True)
-                    summ = torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, device=dev)
+                    d_in.copy_(host_in, non_blocking=True)
                 _lib.check(self.lib.sk_saw_multi(
                     self.L, self.n, d_in[0].data_ptr(), d_in[1].data_ptr(), R, int(begin), int(cnt),
                     summ.data_ptr(), st.cuda_stream,
                 ))
                 with torch.cuda.stream(st):
-                    h = torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)
                     h.copy_(summ, non_blocking=True)
-                outs.append((h, d_in, summ))
+                outs.append((h,))
         for st in self.streams:
             st.synchronize()
         wins, steps = [], []
