@@ -3,7 +3,7 @@ of the paper's stopping model, from device-concurrent
 target campaigns.
 
     python tools/time_to_target.py --lengths 71,75,79,101,121 --reps 100
-    python tools/time_to_target.py --direct 171 --max-runtime 900
+    python tools/time_to_target.py --direct 171,185 --direct-seeds 3 --max-runtime 900
 
 Targets per L: the exact optimum from the device exhaustive scan (L <= 87),
 else the published best-known energy (L >= 171, published.py), else the best
@@ -43,9 +43,11 @@ def main():
     ap.add_argument("--budget-factor", type=float, default=30.0, help="per-rep NSE budget = factor / lambda_model")
     ap.add_argument("--cpu-nse-per-s", type=float, default=9.0e7,
                     help="host reference rate (bench.py --impl reference on the GPU box, L=201)")
-    ap.add_argument("--direct", type=int, default=0)
+    ap.add_argument("--direct", default="", help="comma-separated L with a published target")
+    ap.add_argument("--direct-seeds", type=int, default=1)
     ap.add_argument("--max-runtime", type=float, default=900.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--exhaustive-max-d", type=int, default=40, help="largest D whose target comes from the scan")
     a = ap.parse_args()
 
     import torch
@@ -57,26 +59,28 @@ def main():
     torch.cuda.init()
     points = []
     if a.direct:
-        L = a.direct
-        row = published.best_known(L)
-        if row is None:
-            raise SystemExit(f"no published target for L={L}")
-        t0 = time.monotonic()
-        rec = solve(RunConfig(L=L, walkers=1 << 20, walk_factor=a.walk_factor, master_seed=a.seed,
-                              target_E=row.E, max_runtime=a.max_runtime))
-        dt = time.monotonic() - t0
-        print(json.dumps({"mode": "direct", "L": L, "target_E": row.E, "reached": rec.stop_reason == "target_reached",
-                          "best_E": rec.best_E, "best_hex": rec.best_hex, "seconds": dt,
-                          "total_nses": rec.total_nses, "nse_per_s": rec.total_nses / dt,
-                          "model_expected_nses": 1.0 / stats.PUBLISHED_TREND.rate(L),
-                          "cpu_predicted_seconds": rec.total_nses / (a.cpu_nse_per_s * 101.0 / ((L + 1) // 2))}),
-              flush=True)
+        for L in [int(x) for x in a.direct.split(",") if x]:
+            row = published.best_known(L)
+            if row is None:
+                raise SystemExit(f"no published target for L={L}")
+            for seed in range(a.seed, a.seed + a.direct_seeds):
+                t0 = time.monotonic()
+                rec = solve(RunConfig(L=L, walkers=1 << 20, walk_factor=a.walk_factor, master_seed=seed,
+                                      target_E=row.E, max_runtime=a.max_runtime))
+                dt = time.monotonic() - t0
+                print(json.dumps({"mode": "direct", "L": L, "seed": seed, "target_E": row.E,
+                                  "reached": rec.stop_reason == "target_reached", "best_E": rec.best_E,
+                                  "best_hex": rec.best_hex, "seconds": dt, "total_nses": rec.total_nses,
+                                  "nse_per_s": rec.total_nses / dt,
+                                  "model_expected_nses": 1.0 / stats.PUBLISHED_TREND.rate(L),
+                                  "cpu_predicted_seconds": rec.total_nses / (a.cpu_nse_per_s * 101.0 / ((L + 1) // 2))}),
+                      flush=True)
         return
 
     for L in [int(x) for x in a.lengths.split(",") if x]:
         D = (L + 1) // 2
         lam_model = stats.PUBLISHED_TREND.rate(L)
-        if D <= MAX_EXHAUSTIVE_D and D <= 40:
+        if D <= MAX_EXHAUSTIVE_D and D <= a.exhaustive_max_d:
             t0 = time.monotonic()
             target = exhaustive_optimum(L)[0].E
             source, tsrc = "exhaustive optimum (device scan)", time.monotonic() - t0
