@@ -26,7 +26,8 @@
 //   A regs {a0,a1,a2,a3} = G pairs at x, x-8, x+8, x  with x = 16m + 2t - g,
 //   so consecutive m share one pair (2 new LDS.32 per MMA); G is stored twice
 //   (shifted by one half) so every pair is a 4-byte aligned load.
-//   B regs {b0,b1} = signal pairs at 16(a+m) + 2t + {0, 8}.
+//   B regs {b0,b1} = signal pairs at 16(a+m) + 2t + {0, 8}, stored adjacently
+//   (sig_perm) so that both come from one LDS.64.
 //   D regs {c0..c3} = rows g, g+8 x columns 2t, 2t+1 of each 8-column tile.
 #pragma once
 #include <cuda_fp16.h>
@@ -45,6 +46,16 @@ struct FastGeom {
   uint32_t ext_halves;
 };
 
+// The signal arrays start 32-byte aligned (after both G copies), so that each
+// 16-element block is one aligned 32-byte unit.
+__host__ __device__ inline int sig_off(const FastGeom& g) { return (2 * g.GLEN + 2 + 15) / 16 * 16; }
+
+// Within a 16-element signal block, element u is stored at sig_perm(u): the
+// B-fragment elements of lane t (u = 2t, 2t+1, 2t+8, 2t+9) become the four
+// consecutive halves 4t..4t+3, loaded with one LDS.64.
+__host__ __device__ inline int sig_perm(int u) { return 4 * ((u & 7) >> 1) + 2 * (u >> 3) + (u & 1); }
+__host__ __device__ inline int sig_index(int i) { return (i & ~15) + sig_perm(i & 15); }
+
 __host__ __device__ inline FastGeom fast_geom(int L) {
   FastGeom g;
   const int D = (L + 1) / 2;
@@ -59,9 +70,17 @@ __host__ __device__ inline FastGeom fast_geom(int L) {
   g.GLEN = (g.GLEN + 31) / 64 * 64 + 32;  // copy 2 sits 16 banks away from copy 1
   g.SPAD = 16 * (g.NB - 1) + 16;
   g.SLEN = g.SPAD + 16 * (g.NI + g.NB) + 32;
-  g.SLEN = (g.SLEN + 55) / 64 * 64 + 8;   // S_1 sits 4 banks away from S_0: B loads conflict-free
-  g.ext_halves = uint32_t(g.GLEN + (g.GLEN + 2) + 2 * g.SLEN + ((D + 1) & ~1));
+  // S_1 starts 32*NB bytes (mod 128) after S_0: the first 16 lanes of a B load
+  // read S_0 blocks 0..NB-1 and S_1 blocks 0.. side by side, without conflicts
+  g.SLEN = (g.SLEN + 63) / 64 * 64 + (16 * g.NB) % 64;
+  g.ext_halves = uint32_t(sig_off(g) + 2 * g.SLEN + ((D + 1) & ~1));
   return g;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
@@ -91,19 +110,24 @@ struct EvalFast {
   uint32_t a_addr;      // shared byte address of this lane's A pair at x0 = 2t - g, m = MLO
   uint32_t b_addr[MT];  // shared byte address of this lane's B pair, m = MLO
   // per accumulator slot (nt, o): neighbour h (clamped to >= 0) and its constants
+  // The selection key ((dE/8 + 2^20) << 9) | h equals 64 dE + 2^29 + h, so the
+  // epilogue accumulates the key directly (every term pre-scaled by 64):
+  //   key = Rk - sx * sq2k - xsp64 * X + xq64 * C_{q-p}
   int hc[MT][4];
   uint32_t inv[MT][4];  // 0 for a live slot, ~0 for padding
-  int32_t R[MT][4];     // sum_j s_{h-2j} s_{h+2j}
-  int32_t xsp[MT][4];   // xm * s_h  (xm = 8, 4 at the centre, 0 for padding)
-  int32_t sqv[MT][4];   // s_{L-1-h} (0 at the centre / padding)
-  int32_t c16[MT][4];   // 16 * (K - 1 - pi), 16 * (h >> 1) at the centre
-  int32_t xq[MT][4];    // xm * s_q s_p (= +-8; 0 at the centre / padding)
+  int32_t Rk[MT][4];    // 64*c0 + 2048*R_h + 2^29 + h;  R_h = sum_j s_{h-2j} s_{h+2j},
+                        // c0 = 16 (K - 1 - pi)  (16 (h >> 1) at the centre)
+  int32_t xsp64[MT][4]; // 64 * xm * s_h  (xm = 8, 4 at the centre, 0 for padding)
+  int32_t sq2k[MT][4];  // 2048 * s_{L-1-h} (0 at the centre / padding)
+  int32_t xq64[MT][4];  // 64 * xm * s_q s_p (= +-512; 0 at the centre / padding)
+  int hpar[MT][4];      // h & 1 for live non-centre slots, 2 otherwise (R update mask)
   uint32_t key[MT][4];
   int32_t ce[CPL];      // C_{2j}, j = 1 + lane + 32 r (lag-owned)
 
   static uint32_t ext_bytes(int L, int) { return fast_geom(L).ext_halves * 2u; }
   static bool supports(int L) { return L >= 3 && L <= SK_MAX_L; }
   static constexpr bool kNeedsDl = false;
+  static constexpr bool kSmemKeysVariant = (MT == 1);  // L <= 255: also built with compile-time smem probes
   static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
   static constexpr int kMinBlocks = MT == 1 ? 4 : (MT == 2 ? 3 : 2);  // register caps chosen by measurement
   static int span_hi(int L, int D) { return L - 1 + (D - 1); }  // p + 2K
@@ -114,7 +138,7 @@ struct EvalFast {
     __half* base = reinterpret_cast<__half*>(sm.ext);
     ga = base;
     gb = ga + G.GLEN;
-    sp0 = gb + G.GLEN + 2;
+    sp0 = base + sig_off(G);
     sp1 = sp0 + G.SLEN;
     ces = reinterpret_cast<int16_t*>(sp1 + G.SLEN);
     const __half z = __ushort_as_half(0);
@@ -130,8 +154,8 @@ struct EvalFast {
       }
     }
     for (int i = lane; i < D; i += 32) {
-      sp0[G.SPAD + i] = __int2half_rn(s[2 * i]);                     // S_0[i] = s_{2i}
-      if (i < D - 1) sp1[G.SPAD + i] = __int2half_rn(s[2 * i + 1]);  // S_1[i] = s_{2i+1}
+      sp0[sig_index(G.SPAD + i)] = __int2half_rn(s[2 * i]);                     // S_0[i] = s_{2i}
+      if (i < D - 1) sp1[sig_index(G.SPAD + i)] = __int2half_rn(s[2 * i + 1]);  // S_1[i] = s_{2i+1}
     }
     const int g = lane >> 2, t = lane & 3;
     const int x0 = 2 * t - g + 16 * G.MLO;
@@ -141,7 +165,7 @@ struct EvalFast {
       const int c = 8 * nt + g;
       const int pi = c / G.NB, a = c - pi * G.NB;
       const __half* sb = pi == 1 ? sp1 : sp0;  // columns past 2*NB are padding: any signal will do
-      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * (a + G.MLO) : 0) + 2 * t));
+      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * (a + G.MLO) : 0) + 4 * t));
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int cc = 8 * nt + 2 * t + (o & 1);
@@ -155,13 +179,14 @@ struct EvalFast {
         int32_t r = 0;
         if (ok && !centre)
           for (int j = 1; j <= hp; j++) r += int32_t(s[h - 2 * j]) * int32_t(s[h + 2 * j]);
-        R[nt][o] = r;
         const int32_t sp = ok ? int32_t(s[h]) : 0;
         const int32_t qs = ((D - 1 - h) & 1) ? -1 : 1;  // s_{L-1-h} = qs * s_h (skew symmetry)
-        xsp[nt][o] = (centre ? 4 : 8) * sp;
-        sqv[nt][o] = centre ? 0 : qs * sp;
-        c16[nt][o] = ok ? 16 * (centre ? (h >> 1) : (K - 1 - (h & 1))) : 0;
-        xq[nt][o] = (ok && !centre) ? 8 * qs : 0;
+        const int32_t c0 = ok ? 16 * (centre ? (h >> 1) : (K - 1 - (h & 1))) : 0;
+        Rk[nt][o] = 64 * c0 + 2048 * r + (1 << 29) + (ok ? h : 0);
+        xsp64[nt][o] = 64 * (centre ? 4 : 8) * sp;
+        sq2k[nt][o] = centre ? 0 : 2048 * qs * sp;
+        xq64[nt][o] = (ok && !centre) ? 512 * qs : 0;
+        hpar[nt][o] = (ok && !centre) ? (h & 1) : 2;
       }
     }
     __syncwarp();
@@ -182,7 +207,10 @@ struct EvalFast {
     const uint32_t p0 = lds32(aa), p1 = lds32(aa + 16u);
 #pragma unroll
     for (int nt = 0; nt < MT; nt++)
-      if (nt == 0 || nt < G.NT) mma16816(acc[nt], p0, pm, p1, p0, lds32(bb[nt]), lds32(bb[nt] + 16u));
+      if (nt == 0 || nt < G.NT) {
+        const uint2 b = lds64(bb[nt]);
+        mma16816(acc[nt], p0, pm, p1, p0, b.x, b.y);
+      }
     pm = p1;
   }
 
@@ -224,7 +252,8 @@ struct EvalFast {
       }
     }
 
-    // dE(h) = 16 (c0 + 2R - 2 s_x s_q) - xm s_p (X - s_q C_{q-p})   (see header)
+    // dE(h) = 16 (c0 + 2R - 2 s_x s_q) - xm s_p (X - s_q C_{q-p})   (see header),
+    // accumulated as key = 64 dE + 2^29 + h
     const int K = P.K;
     const int8_t* sx0 = s - 2 * K;   // sx0[3h] = s_{3h-2K} = s_{p-(q-p)} (zero padded)
     const int16_t* cx0 = ces + K;    // cx0[-h] = C_{q-p}
@@ -236,9 +265,9 @@ struct EvalFast {
         const int32_t X = __float2int_rn(accA[nt][o] + accB[nt][o]);
         const int32_t cx = cx0[-h];
         const int32_t sx = sx0[3 * h];
-        const int32_t delta = c16[nt][o] + 32 * (R[nt][o] - sx * sqv[nt][o]) - xsp[nt][o] * X + xq[nt][o] * cx;
-        if (trace_row && !inv[nt][o]) trace_row[h] = delta;
-        key[nt][o] = ((uint32_t((delta >> 3) + kBias) << kHBits) + uint32_t(h)) | inv[nt][o];
+        const int32_t k = Rk[nt][o] - sx * sq2k[nt][o] - xsp64[nt][o] * X + xq64[nt][o] * cx;
+        if (trace_row && !inv[nt][o]) trace_row[h] = (k - (1 << 29) - h) >> 6;
+        key[nt][o] = uint32_t(k) | inv[nt][o];
       }
     }
   }
@@ -267,12 +296,13 @@ struct EvalFast {
     const int32_t sp = s[p];
     const int32_t sq = s[q];
     const int csh = centre ? 1 : 0;      // centre: s_{p+k} = s_{p-k}, so v = (sum) / 2
-    const int32_t sp4 = 4 * sp;
-    // The lag k = q - p excludes its s_{p+k} = s_q term: s_q is zeroed for the
-    // duration of the update (it is overwritten with -s_q below), so every
-    // lane loads s_{p+k} unconditionally.
+    const int32_t nsp4 = -4 * sp;
+    // s_p and s_q are zeroed for the duration of the update (they are
+    // overwritten with -s_p, -s_q below).  Then the lag k = q - p, whose
+    // s_{p+k} = s_q term is excluded, needs no test, and neither does the R
+    // update's own-slot term s_p s_{2h-p} at h = p.
     __syncwarp();
-    if (lane == 0 && !centre) s[q] = 0;
+    if (lane < 2) s[lane ? q : p] = 0;
     __syncwarp();
     // C_k -= 4 v_k(h*) for every even lag (apply_neighbor, _kernels.py:126-158);
     // lags with v_k = 0 leave C_k and its copies untouched
@@ -284,27 +314,28 @@ struct EvalFast {
       const int32_t b = s[p + k];
       const int32_t v = (a + b) >> csh;
       if (v != 0 && j <= K) {
-        ce[r] -= sp4 * v;
+        ce[r] += nsp4 * v;
         ces[j] = int16_t(ce[r]);
         write_g(j, ce[r]);
       }
     }
-    // R_h: the terms s_x s_{2h-x} with x in {p, q} change sign.  Out-of-range
-    // partners read the zero padding; x = h (own flip) and the centre's
-    // coincident pair are masked.  A flip of h itself negates s_h and s_{L-1-h}.
+    // R_h: the terms s_x s_{2h-x} with x in {p, q} change sign (same-parity,
+    // live, non-centre slots).  Out-of-range partners read the zero padding,
+    // the own-slot pair (x = h = p) reads the zeroed s_p, and a centre move
+    // flips only x = p.  A flip of h itself negates s_h and s_{L-1-h}.
     const int pp = p & 1;
+    const int32_t sp4k = 4096 * sp, sq4k = centre ? 0 : 4096 * sq;
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int h = hc[nt][o];
-        const bool own = (h == p) && !inv[nt][o];
-        const bool act = ((h & 1) == pp) && (sqv[nt][o] != 0);  // live, non-centre, same parity
-        const int32_t v1 = own ? 0 : int32_t(s[2 * h - p]);
-        const int32_t v2 = centre ? 0 : int32_t(s[2 * h - q]);
-        R[nt][o] -= act ? 2 * (sp * v1 + sq * v2) : 0;
-        xsp[nt][o] = own ? -xsp[nt][o] : xsp[nt][o];
-        sqv[nt][o] = own ? -sqv[nt][o] : sqv[nt][o];
+        const bool own = (h == p);  // padding slots have xsp64 = sq2k = 0: negating them is harmless
+        const int32_t v1 = s[2 * h - p];
+        const int32_t v2 = s[2 * h - q];
+        Rk[nt][o] -= (hpar[nt][o] == pp) ? sp4k * v1 + sq4k * v2 : 0;
+        xsp64[nt][o] = own ? -xsp64[nt][o] : xsp64[nt][o];
+        sq2k[nt][o] = own ? -sq2k[nt][o] : sq2k[nt][o];
       }
     }
     __syncwarp();
@@ -312,7 +343,7 @@ struct EvalFast {
       const int x = lane ? q : p;
       const int32_t sx = lane ? sq : sp;
       s[x] = int8_t(-sx);
-      ((x & 1) ? sp1 : sp0)[G.SPAD + (x >> 1)] = __int2half_rn(-sx);
+      ((x & 1) ? sp1 : sp0)[sig_index(G.SPAD + (x >> 1))] = __int2half_rn(-sx);
     }
     __syncwarp();
   }

@@ -34,6 +34,7 @@ struct EvalScalar {
   static constexpr uint32_t ext_bytes(int, int) { return 0; }
   static bool supports(int) { return true; }
   static constexpr bool kNeedsDl = true;
+  static constexpr bool kSmemKeysVariant = false;
   static constexpr bool kCeAliasKeys = false;
   static constexpr int kMinBlocks = 1;
   static int span_hi(int L, int) { return 2 * L - 2; }  // q + k

@@ -154,6 +154,15 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   } else {
     pl.P.gkeys = nullptr;
   }
+  if constexpr (Eval::kSmemKeysVariant && !TRACE) {
+    if (keys_in_smem) {  // compile-time shared-memory probes for the production kernels
+      auto kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 1>;
+      SK_CUDA(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      kern_s<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
+      SK_CUDA(cudaGetLastError());
+      return SK_OK;
+    }
+  }
   SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
   SK_CUDA(cudaGetLastError());

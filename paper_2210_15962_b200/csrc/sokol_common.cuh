@@ -126,8 +126,10 @@ struct VisitedSet {
   __device__ __forceinline__ void bind_shared() {
     keys_s = __isShared(keys) ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
   }
+  // KS = 1: keys are known (at compile time) to live in shared memory.
+  template <int KS>
   __device__ __forceinline__ uint64_t load_key(uint32_t slot) const {
-    if (keys_s) {  // explicit LDS: generic loads of shared data cost extra latency on the probe path
+    if (KS == 1 || keys_s) {  // explicit LDS: generic loads of shared data cost extra latency on the probe path
       uint64_t v;
       asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(keys_s + slot * 8u));
       return v;
@@ -147,6 +149,7 @@ struct VisitedSet {
 
   // Warp-collective.  Returns true iff u is present.  If absent and
   // `insert_if_absent`, the lane at the first free slot writes it.
+  template <int KS = 0>
   __device__ __forceinline__ bool probe(uint64_t key, int lane, bool insert_if_absent) {
     uint32_t start = home(key, shift);
     for (;;) {
@@ -155,13 +158,13 @@ struct VisitedSet {
       const uint32_t empty_mask = __ballot_sync(kFull, !used);
       // lanes strictly before the first empty slot are the live probe run
       const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
-      const bool hit = ((run >> lane) & 1u) && load_key(slot) == key;
+      const bool hit = ((run >> lane) & 1u) && load_key<KS>(slot) == key;
       if (__any_sync(kFull, hit)) return true;
       if (empty_mask) {
         if (insert_if_absent) {
           const int first = __ffs(empty_mask) - 1;
           if (lane == first) {
-            if (keys_s)
+            if (KS == 1 || keys_s)
               asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys_s + slot * 8u), "l"(key) : "memory");
             else
               keys[slot] = key;

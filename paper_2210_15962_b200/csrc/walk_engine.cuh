@@ -82,8 +82,9 @@ struct SmemLayout {
     if (need_dl) o = align_up(o + 4u * uint32_t(D), 16);
     s.off_occ = o;
     o = align_up(o + 4u * (cap / 32u), 16);
+    o = align_up(o, 32);  // evaluator area 32-byte aligned (signal blocks are 32-byte units)
     s.off_ext = o;
-    o = align_up(o + ext_bytes, 16);
+    o = align_up(o + ext_bytes, 32);  // every warp's area starts 32-byte aligned
     s.total = o;
     return s;
   }
@@ -91,7 +92,8 @@ struct SmemLayout {
 
 constexpr int32_t kExcluded = 0x7fffffff;
 
-template <int NW, bool TRACE, class Eval>
+// KS = 1: the visited keys are in shared memory (compile-time; see VisitedSet)
+template <int NW, bool TRACE, class Eval, int KS>
 __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayout& lay, char* wbase,
                                              uint64_t* gkeys_warp, int64_t w, int lane) {
   const int L = P.L, D = P.D, K = P.K, n = P.n;
@@ -159,7 +161,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   __syncwarp();
   KeyState<NW> ks;
   ks.init(words);
-  vs.probe(ks.u_of(words), lane, true);
+  vs.probe<KS>(ks.u_of(words), lane, true);
 
   int32_t best_e = E;
   uint64_t best_w[NW];
@@ -194,7 +196,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
       }
       uint64_t chain[NW];
       const uint64_t nk = ks.u_of_flip(words, D, hc, chain);
-      if (!vs.probe(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
+      if (!vs.probe<KS>(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
         hs = hc;
         dsel = cand_delta(m);
         ks.commit(D, hc, chain);
@@ -247,16 +249,16 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   __syncwarp();
 }
 
-template <int NW, bool TRACE, class Eval, int WPB>
+template <int NW, bool TRACE, class Eval, int WPB, int KS = 0>
 __global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(WalkParams P, SmemLayout lay) {
-  extern __shared__ __align__(16) char smem_raw[];
+  extern __shared__ __align__(128) char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = int64_t(blockIdx.x) * WPB + wib;
   const int64_t nwarps = int64_t(gridDim.x) * WPB;
   char* wbase = smem_raw + size_t(wib) * P.warp_smem;
   uint64_t* gkeys = P.gkeys ? P.gkeys + size_t(gwarp) * P.cap : nullptr;
-  for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval>(P, lay, wbase, gkeys, w, lane);
+  for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval, KS>(P, lay, wbase, gkeys, w, lane);
 }
 
 // Summary init / finish (tiny kernels on the same stream), one block per
