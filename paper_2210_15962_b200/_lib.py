@@ -13,7 +13,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsokol.so")
+# SOKOL_LIB: load an alternative in-tree build (kernel experiments, tools/); default libsokol.so
+LIB_PATH = os.environ.get("SOKOL_LIB") or os.path.join(_HERE, "libsokol.so")
 
 SK_OK = 0
 SK_ERR_ARG = -1

@@ -46,10 +46,12 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Compile libsokol.so (or, with `out`/`defines`, an experimental variant)."""
+    if out == OUT and not defines and not force and not stale():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", os.path.join(CSRC, "sokol_abi.cu")]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp",
+           os.path.join(CSRC, "sokol_abi.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -57,11 +59,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-4000:])
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
-        print(f"built {OUT}")
-    return OUT
+        print(f"built {out}")
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python -m paper_2210_15962_b200.build [--force] [--variant NAME -DDEF=V ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        defs = [a[2:] for a in args if a.startswith("-D")]
+        build(verbose=True, out=os.path.join(HERE, f"libsokol_{name}.so"), defines=defs)
+    else:
+        build(force="--force" in args, verbose=True)

@@ -34,6 +34,13 @@
 
 #include "walk_engine.cuh"
 
+// Blocks per SM the L <= 255 kernels are register-capped for (4 x 128 threads:
+// 128 registers; 5: 102).  Chosen by measurement; overridable
+// at build time for experiments.
+#ifndef SK_MT1_MIN_BLOCKS
+#define SK_MT1_MIN_BLOCKS 4
+#endif
+
 namespace sk {
 
 struct FastGeom {
@@ -129,7 +136,7 @@ struct EvalFast {
   static constexpr bool kNeedsDl = false;
   static constexpr bool kSmemKeysVariant = (MT == 1);  // L <= 255: also built with compile-time smem probes
   static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
-  static constexpr int kMinBlocks = MT == 1 ? 4 : (MT == 2 ? 3 : 2);  // register caps chosen by measurement
+  static constexpr int kMinBlocks = MT == 1 ? SK_MT1_MIN_BLOCKS : (MT == 2 ? 3 : 2);  // register caps chosen by measurement
   static int span_hi(int L, int D) { return L - 1 + (D - 1); }  // p + 2K
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {

@@ -75,20 +75,33 @@ struct KeyState {
     const int b = D - 1 - h;
     const int wi = b >> 6;
     const uint64_t bit = 1ull << (b & 63);
-    uint64_t x = hp[0];
+    if constexpr (NW == 1) {
+      return hp[0] ^ w[0] ^ bit;
+    } else if constexpr (NW == 2) {
+      // wi is warp-uniform: a branch, so only the needed path executes
+      if (wi == 1) return hp[1] ^ w[1] ^ bit;
+      chain[1] = mix64(hp[0] ^ w[0] ^ bit);
+      return chain[1] ^ w[1];
+    } else {
+      uint64_t x = hp[0];
 #pragma unroll
-    for (int i = 0; i < NW; i++) {
-      x = (i == wi) ? hp[i] : x;  // prefix unchanged up to the flipped word (selects: no local memory)
-      chain[i] = x;
-      if (i + 1 < NW && i >= wi) x = mix64(x ^ (w[i] ^ (i == wi ? bit : 0ull)));
+      for (int i = 0; i < NW; i++) {
+        x = (i == wi) ? hp[i] : x;  // prefix unchanged up to the flipped word (selects: no local memory)
+        chain[i] = x;
+        if (i + 1 < NW && i >= wi) x = mix64(x ^ (w[i] ^ (i == wi ? bit : 0ull)));
+      }
+      return chain[NW - 1] ^ (w[NW - 1] ^ (wi == NW - 1 ? bit : 0ull));
     }
-    return chain[NW - 1] ^ (w[NW - 1] ^ (wi == NW - 1 ? bit : 0ull));
   }
 
   __device__ __forceinline__ void commit(int D, int h, const uint64_t (&chain)[NW]) {
     const int wi = (D - 1 - h) >> 6;
+    if constexpr (NW == 2) {
+      if (wi == 0) hp[1] = chain[1];
+    } else {
 #pragma unroll
-    for (int i = 1; i < NW; i++) hp[i] = (i > wi) ? chain[i] : hp[i];
+      for (int i = 1; i < NW; i++) hp[i] = (i > wi) ? chain[i] : hp[i];
+    }
   }
 };
 
@@ -96,9 +109,15 @@ template <int NW>
 __device__ __forceinline__ void toggle_half_bit(uint64_t (&w)[NW], int D, int h) {
   const int b = D - 1 - h;
   const uint64_t bit = 1ull << (b & 63);
-  // selects, not a conditional store: a data-dependent index would push w[] to local memory
+  if constexpr (NW == 1) {
+    w[0] ^= bit;
+  } else if constexpr (NW == 2) {
+    if (b >> 6) w[1] ^= bit; else w[0] ^= bit;  // warp-uniform
+  } else {
+    // selects, not a conditional store: a data-dependent index would push w[] to local memory
 #pragma unroll
-  for (int i = 0; i < NW; i++) w[i] ^= ((b >> 6) == i) ? bit : 0ull;
+    for (int i = 0; i < NW; i++) w[i] ^= ((b >> 6) == i) ? bit : 0ull;
+  }
 }
 
 __device__ __forceinline__ uint32_t pack_cand(int32_t delta, int h) {
