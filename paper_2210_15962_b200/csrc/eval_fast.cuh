@@ -40,6 +40,9 @@
 #ifndef SK_MT1_MIN_BLOCKS
 #define SK_MT1_MIN_BLOCKS 4
 #endif
+#ifndef SK_MT2_MIN_BLOCKS
+#define SK_MT2_MIN_BLOCKS 3
+#endif
 
 namespace sk {
 
@@ -77,9 +80,10 @@ __host__ __device__ inline FastGeom fast_geom(int L) {
   g.GLEN = (g.GLEN + 31) / 64 * 64 + 32;  // copy 2 sits 16 banks away from copy 1
   g.SPAD = 16 * (g.NB - 1) + 16;
   g.SLEN = g.SPAD + 16 * (g.NI + g.NB) + 32;
-  // S_1 starts 32*NB bytes (mod 128) after S_0: the first 16 lanes of a B load
-  // read S_0 blocks 0..NB-1 and S_1 blocks 0.. side by side, without conflicts
-  g.SLEN = (g.SLEN + 63) / 64 * 64 + (16 * g.NB) % 64;
+  // S_1 starts 64 bytes (mod 128) after S_0: each half-warp of a B load reads
+  // two S_0 blocks and the same two S_1 blocks (column map below), side by
+  // side in the banks
+  g.SLEN = (g.SLEN + 63) / 64 * 64 + 32;
   g.ext_halves = uint32_t(sig_off(g) + 2 * g.SLEN + ((D + 1) & ~1));
   return g;
 }
@@ -127,7 +131,8 @@ struct EvalFast {
   int32_t xsp64[MT][4]; // 64 * xm * s_h  (xm = 8, 4 at the centre, 0 for padding)
   int32_t sq2k[MT][4];  // 2048 * s_{L-1-h} (0 at the centre / padding)
   int32_t xq64[MT][4];  // 64 * xm * s_q s_p (= +-512; 0 at the centre / padding)
-  int hpar[MT][4];      // h & 1 for live non-centre slots, 2 otherwise (R update mask)
+  int ridx[MT][4];      // 2h for live non-centre slots; -1 otherwise (R-update reads land in zero padding)
+  int lpar;             // parity of every slot of this lane (column map: pi = t & 1)
   uint32_t key[MT][4];
   int32_t ce[CPL];      // C_{2j}, j = 1 + lane + 32 r (lag-owned)
 
@@ -136,8 +141,14 @@ struct EvalFast {
   static constexpr bool kNeedsDl = false;
   static constexpr bool kSmemKeysVariant = (MT == 1);  // L <= 255: also built with compile-time smem probes
   static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
-  static constexpr int kMinBlocks = MT == 1 ? SK_MT1_MIN_BLOCKS : (MT == 2 ? 3 : 2);  // register caps chosen by measurement
-  static int span_hi(int L, int D) { return L - 1 + (D - 1); }  // p + 2K
+  static constexpr int kMinBlocks = MT == 1 ? SK_MT1_MIN_BLOCKS : (MT == 2 ? SK_MT2_MIN_BLOCKS : 2);  // register caps chosen by measurement
+  // Spin-array margins.  The C update reads s_{p -+ 2j} for every lag slot
+  // j <= 32 CPL (idle slots j > K must read zeros, so they need no test), the
+  // R update reads down to -1 - q, the epilogue up to p + 2K.  CPL follows L
+  // (the tile count of the evaluator the launcher picks for it).
+  static int cpl_for(int D) { return 4 * ((((D + 63) / 64) + 1) / 2); }
+  static int span_hi(int L, int D) { return L - 1 + max(D - 1, 64 * cpl_for(D)); }
+  static int span_lo(int L, int D) { return max(L + 1, 64 * cpl_for(D)); }
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
     G = fast_geom(P.L);
@@ -168,18 +179,23 @@ struct EvalFast {
     const int x0 = 2 * t - g + 16 * G.MLO;
     a_addr = uint32_t(__cvta_generic_to_shared((g & 1) ? gb + G.GOFF + 1 + x0 : ga + G.GOFF + x0));
 #pragma unroll
+    // Column map: column c holds parity pi = (c >> 1) & 1 and output block
+    // a = 2 (c >> 2) + (c & 1).  A lane's accumulator columns 2t, 2t+1 then
+    // share the parity t & 1, so the R update needs no per-slot parity test.
+    lpar = t & 1;
+#pragma unroll
     for (int nt = 0; nt < MT; nt++) {
       const int c = 8 * nt + g;
-      const int pi = c / G.NB, a = c - pi * G.NB;
-      const __half* sb = pi == 1 ? sp1 : sp0;  // columns past 2*NB are padding: any signal will do
-      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (pi < 2 ? 16 * (a + G.MLO) : 0) + 4 * t));
+      const int pi = (c >> 1) & 1, a = 2 * (c >> 2) + (c & 1);
+      const __half* sb = pi == 1 ? sp1 : sp0;  // columns with a >= NB are padding: any signal will do
+      b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (a < G.NB ? 16 * (a + G.MLO) : 0) + 4 * t));
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int cc = 8 * nt + 2 * t + (o & 1);
-        const int ppi = cc / G.NB, aa = cc - ppi * G.NB;
+        const int ppi = (cc >> 1) & 1, aa = 2 * (cc >> 2) + (cc & 1);
         const int hp = 16 * aa + g + 8 * (o >> 1);
         const int h = 2 * hp + ppi;
-        const bool ok = nt < G.NT && ppi < 2 && h < D;
+        const bool ok = nt < G.NT && aa < G.NB && h < D;
         const bool centre = ok && h == K;
         hc[nt][o] = ok ? h : 0;
         inv[nt][o] = ok ? 0u : ~0u;
@@ -193,7 +209,7 @@ struct EvalFast {
         xsp64[nt][o] = 64 * (centre ? 4 : 8) * sp;
         sq2k[nt][o] = centre ? 0 : 2048 * qs * sp;
         xq64[nt][o] = (ok && !centre) ? 512 * qs : 0;
-        hpar[nt][o] = (ok && !centre) ? (h & 1) : 2;
+        ridx[nt][o] = (ok && !centre) ? 2 * h : -1;
       }
     }
     __syncwarp();
@@ -316,11 +332,11 @@ struct EvalFast {
 #pragma unroll
     for (int r = 0; r < CPL; r++) {
       const int j = 1 + lane + 32 * r;
-      const int k = 2 * min(j, K);  // clamped so idle lanes read inside the padded span
+      const int k = 2 * j;  // idle slots (j > K) read the zero margins: v = 0
       const int32_t a = s[p - k];
       const int32_t b = s[p + k];
       const int32_t v = (a + b) >> csh;
-      if (v != 0 && j <= K) {
+      if (v != 0) {
         ce[r] += nsp4 * v;
         ces[j] = int16_t(ce[r]);
         write_g(j, ce[r]);
@@ -330,17 +346,19 @@ struct EvalFast {
     // live, non-centre slots).  Out-of-range partners read the zero padding,
     // the own-slot pair (x = h = p) reads the zeroed s_p, and a centre move
     // flips only x = p.  A flip of h itself negates s_h and s_{L-1-h}.
-    const int pp = p & 1;
-    const int32_t sp4k = 4096 * sp, sq4k = centre ? 0 : 4096 * sq;
+    // Centre and padding slots have ridx = -1, so both reads hit the zero
+    // padding below position 0; other-parity lanes get zero weights.
+    const bool same = (lpar == (p & 1));
+    const int32_t sp4k = same ? 4096 * sp : 0, sq4k = (same && !centre) ? 4096 * sq : 0;
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int h = hc[nt][o];
         const bool own = (h == p);  // padding slots have xsp64 = sq2k = 0: negating them is harmless
-        const int32_t v1 = s[2 * h - p];
-        const int32_t v2 = s[2 * h - q];
-        Rk[nt][o] -= (hpar[nt][o] == pp) ? sp4k * v1 + sq4k * v2 : 0;
+        const int32_t v1 = s[ridx[nt][o] - p];
+        const int32_t v2 = s[ridx[nt][o] - q];
+        Rk[nt][o] -= sp4k * v1 + sq4k * v2;
         xsp64[nt][o] = own ? -xsp64[nt][o] : xsp64[nt][o];
         sq2k[nt][o] = own ? -sq2k[nt][o] : sq2k[nt][o];
       }

@@ -38,6 +38,7 @@ struct EvalScalar {
   static constexpr bool kCeAliasKeys = false;
   static constexpr int kMinBlocks = 1;
   static int span_hi(int L, int) { return 2 * L - 2; }  // q + k
+  static int span_lo(int L, int) { return L - 1; }      // p - k
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 

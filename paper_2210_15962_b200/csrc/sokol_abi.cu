@@ -113,9 +113,9 @@ Plan make_plan(int L, int n) {
   pl.P.cap = visited_capacity(n);
   pl.smem_keys_ok = pl.P.cap * 8u <= kSmemKeysMax;
   pl.lay_s = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, true, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                  Eval::span_hi(L, D), Eval::kCeAliasKeys);
+                                  Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
   pl.lay_g = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, false, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                  Eval::span_hi(L, D), Eval::kCeAliasKeys);
+                                  Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
   return pl;
 }
 

@@ -62,10 +62,11 @@ struct SmemLayout {
   // ce_alias_keys: the int32 C array is only read during init, so it may share
   // the visited-set key storage (cleared after init) when that is in smem.
   __host__ __device__ static SmemLayout make(int L, int K, int D, uint32_t cap, bool keys_in_smem,
-                                             uint32_t ext_bytes, bool need_dl, int span_hi, bool ce_alias_keys) {
+                                             uint32_t ext_bytes, bool need_dl, int span_hi, bool ce_alias_keys,
+                                             int span_lo) {
     SmemLayout s;
-    s.span_off = L - 1;
-    s.span = uint32_t(L - 1 + span_hi + 1);
+    s.span_off = span_lo;  // zero cells below position 0 (>= L + 1, see the evaluators' span_lo)
+    s.span = uint32_t(span_lo + span_hi + 1);
     const bool alias = ce_alias_keys && keys_in_smem && cap * 8u >= 4u * uint32_t(K + 1);
     uint32_t o = 0;
     s.off_keys = o;
@@ -105,7 +106,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   sm.occ = reinterpret_cast<uint32_t*>(wbase + lay.off_occ);
   sm.keys = gkeys_warp ? gkeys_warp : reinterpret_cast<uint64_t*>(wbase + lay.off_keys);
   sm.ext = wbase + lay.off_ext;
-  int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-(L-1), span_hi], zero outside [0, L)
+  int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-span_lo, span_hi], zero outside [0, L)
 
   // ---- first pivot (_kernels.py:201-209) --------------------------------
   uint64_t master = P.master, batch = P.batch;
