@@ -84,7 +84,8 @@ __host__ __device__ inline FastGeom fast_geom(int L) {
   // two S_0 blocks and the same two S_1 blocks (column map below), side by
   // side in the banks
   g.SLEN = (g.SLEN + 63) / 64 * 64 + 32;
-  g.ext_halves = uint32_t(sig_off(g) + 2 * g.SLEN + ((D + 1) & ~1));
+  // ... + ces (int16 C copy, D entries) + flip table (2 x D uint16 byte offsets)
+  g.ext_halves = uint32_t(sig_off(g) + 2 * g.SLEN + ((D + 1) & ~1) + 2 * D);
   return g;
 }
 
@@ -118,6 +119,7 @@ struct EvalFast {
   __half* sp0;
   __half* sp1;
   int16_t* ces;         // int16 copy of C_{2j}, read by the epilogue (C_{q-p})
+  uint16_t* flipoff;    // [2][D]: byte offset (from sp0) of the signal cell of p = h / q = L-1-h
   uint32_t a_addr;      // shared byte address of this lane's A pair at x0 = 2t - g, m = MLO
   uint32_t b_addr[MT];  // shared byte address of this lane's B pair, m = MLO
   // per accumulator slot (nt, o): neighbour h (clamped to >= 0) and its constants
@@ -159,6 +161,7 @@ struct EvalFast {
     sp0 = base + sig_off(G);
     sp1 = sp0 + G.SLEN;
     ces = reinterpret_cast<int16_t*>(sp1 + G.SLEN);
+    flipoff = reinterpret_cast<uint16_t*>(ces + ((D + 1) & ~1));
     const __half z = __ushort_as_half(0);
     for (uint32_t i = lane; i < G.ext_halves; i += 32) base[i] = z;
     __syncwarp();
@@ -174,6 +177,11 @@ struct EvalFast {
     for (int i = lane; i < D; i += 32) {
       sp0[sig_index(G.SPAD + i)] = __int2half_rn(s[2 * i]);                     // S_0[i] = s_{2i}
       if (i < D - 1) sp1[sig_index(G.SPAD + i)] = __int2half_rn(s[2 * i + 1]);  // S_1[i] = s_{2i+1}
+    }
+    for (int i = lane; i < 2 * D; i += 32) {  // position x -> its signal cell, for the flips of a move
+      const int h = i < D ? i : i - D;
+      const int x = i < D ? h : P.L - 1 - h;
+      flipoff[i] = uint16_t(2 * ((x & 1) * G.SLEN + sig_index(G.SPAD + (x >> 1))));
     }
     const int g = lane >> 2, t = lane & 3;
     const int x0 = 2 * t - g + 16 * G.MLO;
@@ -368,7 +376,12 @@ struct EvalFast {
       const int x = lane ? q : p;
       const int32_t sx = lane ? sq : sp;
       s[x] = int8_t(-sx);
-      ((x & 1) ? sp1 : sp0)[sig_index(G.SPAD + (x >> 1))] = __int2half_rn(-sx);
+      const uint16_t half_bits = sx > 0 ? 0xBC00u : 0x3C00u;  // f16 of -sx
+      if constexpr (MT == 1) {  // table lookup (measured faster for MT = 1, slower for MT = 2)
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(sp0) + flipoff[lane * P.D + p]) = half_bits;
+      } else {
+        reinterpret_cast<uint16_t*>((x & 1) ? sp1 : sp0)[sig_index(G.SPAD + (x >> 1))] = half_bits;
+      }
     }
     __syncwarp();
   }

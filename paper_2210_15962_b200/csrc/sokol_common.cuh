@@ -173,11 +173,15 @@ struct VisitedSet {
     uint32_t start = home(key, shift);
     for (;;) {
       const uint32_t slot = (start + lane) & mask;
-      const bool used = (occ[slot >> 5] >> (slot & 31)) & 1u;
+      const uint32_t ow = occ[slot >> 5];
+      // shared-memory keys: load the slot's key alongside its occupancy word
+      // (stale keys of free slots are masked by `run` below)
+      const uint64_t kv = KS == 1 ? load_key<1>(slot) : 0ull;
+      const bool used = (ow >> (slot & 31)) & 1u;
       const uint32_t empty_mask = __ballot_sync(kFull, !used);
       // lanes strictly before the first empty slot are the live probe run
       const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
-      const bool hit = ((run >> lane) & 1u) && load_key<KS>(slot) == key;
+      const bool hit = ((run >> lane) & 1u) && (KS == 1 ? kv == key : load_key<KS>(slot) == key);
       if (__any_sync(kFull, hit)) return true;
       if (empty_mask) {
         if (insert_if_absent) {
