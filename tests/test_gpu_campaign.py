@@ -134,3 +134,16 @@ def test_checkpoint_resume_equals_uninterrupted(tmp_path, golden_records):
     # a checkpoint of another search is refused
     with pytest.raises(ValueError):
         solve(RunConfig(**{**item["config"], "master_seed": 12345}), checkpoint=ck)
+
+
+def test_speculative_batches_change_nothing(oracle):
+    # min_walks_per_launch=1 disables speculation; a large value runs up to 64
+    # batches of every repetition per launch and discards those after its stop
+    cfg = RunConfig(L=45, walkers=3, master_seed=13, target_E=118, max_nses=200_000)
+    plain = target_campaign(cfg, 12, min_walks_per_launch=1)
+    spec = target_campaign(cfg, 12, min_walks_per_launch=1 << 20)
+    assert plain.nses == spec.nses and plain.censored == spec.censored
+    assert plain.censored_count == 6  # both outcomes occur (oracle: 6 of 12 reach the optimum)
+    for rep in range(12):
+        rec = oracle.solve_record(45, 3, 8, derive_repetition_seed(13, rep), 200_000, 118)
+        assert spec.nses[rep] == rec["total_nses"]
