@@ -287,9 +287,9 @@ int exh_validate(int L) {
 // O(L^2) state rebuild, short enough to give every SM work
 int exh_chunk_log2(int D) { return std::max(4, std::min(16, D - 19)); }
 
-template <int KMAX>
+template <int G>
 int exh_launch(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key, cudaStream_t st, int dev) {
-  auto kern = sk::exhaustive_kernel<KMAX>;
+  auto kern = sk::exhaustive_kernel<G>;
   const int cl2 = exh_chunk_log2((L + 1) / 2);
   const uint64_t nchunks = ((g_end - g_begin) + (1ull << cl2) - 1) >> cl2;
   int sms = 0, per = 0;
@@ -302,12 +302,16 @@ int exh_launch(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key,
   return SK_OK;
 }
 
+// lag groups of four: G = ceil(K / 4), bucketed (unused lags are C = 0 bytes)
 int exh_run(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key, cudaStream_t st, int dev) {
   const int K = (L + 1) / 2 - 1;
-  if (K <= 15) return exh_launch<15>(L, g_begin, g_end, key, st, dev);
-  if (K <= 23) return exh_launch<23>(L, g_begin, g_end, key, st, dev);
-  if (K <= 31) return exh_launch<31>(L, g_begin, g_end, key, st, dev);
-  return exh_launch<43>(L, g_begin, g_end, key, st, dev);
+  const int G = (K + 3) / 4;
+  if (G <= 4) return exh_launch<4>(L, g_begin, g_end, key, st, dev);
+  if (G <= 6) return exh_launch<6>(L, g_begin, g_end, key, st, dev);
+  if (G <= 8) return exh_launch<8>(L, g_begin, g_end, key, st, dev);
+  if (G <= 9) return exh_launch<9>(L, g_begin, g_end, key, st, dev);
+  if (G <= 10) return exh_launch<10>(L, g_begin, g_end, key, st, dev);
+  return exh_launch<11>(L, g_begin, g_end, key, st, dev);
 }
 
 __global__ void exh_key_init(unsigned long long* k) { *k = ~0ull; }

@@ -21,7 +21,7 @@ with tempfile.TemporaryDirectory() as d:
     subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=d, capture_output=True)
     cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
     txt = subprocess.run(["nvdisasm", "--print-line-info", os.path.join(d, cub)], capture_output=True, text=True).stdout
-sym = f"_ZN2sk15{name}" if not name.startswith("_") else name
+sym = name if name.startswith("_") else (f"_ZN2sk15{name}" if name.startswith("saw_walk") else f"_ZN2sk{len(name.split('I')[0])}{name}")
 start = re.search(r"\n\.text\." + re.escape(sym) + r"[^:\n]*:", txt).start()
 body = txt[start:]
 nxt = body.find("\n.text.", 10)
