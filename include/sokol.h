@@ -59,6 +59,18 @@ int sk_set_variant(int variant);
 int sk_get_variant(void);
 
 /*
+ * Visited-set layout of subsequent walk launches (process-global).  AUTO
+ * picks by occupancy; SMEM keeps the 64-bit keys in shared memory;
+ * FINGERPRINT keeps 32-bit fingerprints in shared memory and the keys in an
+ * L2-resident global scratch (half the shared memory per walk).  Membership,
+ * and so every result, is identical in all three.
+ */
+#define SK_VISITED_AUTO 0
+#define SK_VISITED_SMEM 1
+#define SK_VISITED_FINGERPRINT 2
+int sk_set_visited_layout(int mode);
+
+/*
  * Batch of independent walks on the current CUDA device, asynchronous on
  * `stream` (a cudaStream_t; NULL = legacy default stream).
  * Replaces skewsaw._kernels.saw_batch(length, n, seeds, best_e_out,

@@ -29,6 +29,10 @@ VARIANT_AUTO = 0
 VARIANT_SCALAR = 1
 VARIANT_FAST = 2
 
+VISITED_AUTO = 0
+VISITED_SMEM = 1
+VISITED_FINGERPRINT = 2
+
 # Every symbol include/sokol.h declares; tests/test_abi.py checks the export
 # table against this list and against the header itself.
 EXPORTS = (
@@ -37,6 +41,7 @@ EXPORTS = (
     "sk_max_length",
     "sk_set_variant",
     "sk_get_variant",
+    "sk_set_visited_layout",
     "sk_saw_batch",
     "sk_saw_multi",
     "sk_saw_trace",
@@ -88,6 +93,8 @@ def _declare(lib):
     lib.sk_set_variant.argtypes = [_i]
     lib.sk_set_variant.restype = _i
     lib.sk_get_variant.restype = _i
+    lib.sk_set_visited_layout.argtypes = [_i]
+    lib.sk_set_visited_layout.restype = _i
     lib.sk_saw_batch.argtypes = [_i, _i, _vp, _u64, _u64, _u64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
     lib.sk_saw_batch.restype = _i
     lib.sk_saw_multi.argtypes = [_i, _i, _vp, _vp, _i, _u64, _i64, _vp, _vp]
@@ -140,3 +147,7 @@ def set_variant(variant: int):
 
 def get_variant() -> int:
     return int(load().sk_get_variant())
+
+
+def set_visited_layout(mode: int):
+    check(load().sk_set_visited_layout(mode))

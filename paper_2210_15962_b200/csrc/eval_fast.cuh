@@ -186,7 +186,6 @@ struct EvalFast {
     const int g = lane >> 2, t = lane & 3;
     const int x0 = 2 * t - g + 16 * G.MLO;
     a_addr = uint32_t(__cvta_generic_to_shared((g & 1) ? gb + G.GOFF + 1 + x0 : ga + G.GOFF + x0));
-#pragma unroll
     // Column map: column c holds parity pi = (c >> 1) & 1 and output block
     // a = 2 (c >> 2) + (c & 1).  A lane's accumulator columns 2t, 2t+1 then
     // share the parity t & 1, so the R update needs no per-slot parity test.

@@ -25,6 +25,7 @@ namespace {
 
 thread_local std::string g_err;
 int g_variant = SK_VARIANT_AUTO;
+int g_visited = SK_VISITED_AUTO;
 std::mutex g_mu;
 
 int fail(int code, const std::string& msg) {
@@ -119,12 +120,20 @@ Plan make_plan(int L, int n) {
   return pl;
 }
 
-// Occupancy-driven placement of the visited keys: shared memory unless moving
-// them to L2 lets more walks be resident (measured: the L2 probes cost less
-// than the occupancy they buy once keys exceed ~8 KB per walk).
+// Occupancy-driven placement of the visited keys: full keys in shared memory,
+// or fingerprints in shared memory with the keys in an L2-resident global
+// scratch, whichever lets more walks be resident (ties: shared memory).  The
+// production kernels (Eval::kSmemKeysVariant, no trace) are compiled for each
+// layout (KS = 1 / 2); the others decide at run time (KS = 0).
 template <int NW, bool TRACE, class Eval>
 int launch_nw(Plan& pl, cudaStream_t st, int dev) {
-  auto kern = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB>;
+  using KernT = void (*)(sk::WalkParams, sk::SmemLayout);
+  KernT kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 0>;
+  KernT kern_g = kern_s;
+  if constexpr (Eval::kSmemKeysVariant && !TRACE) {
+    kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 1>;
+    kern_g = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 2>;
+  }
   int sms = 0, per_s = 0, per_g = 0;
   SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem_s = size_t(pl.lay_s.total) * kWPB, smem_g = size_t(pl.lay_g.total) * kWPB;
@@ -132,11 +141,18 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   SK_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const bool s_ok = pl.smem_keys_ok && smem_s <= size_t(max_optin);
   const bool g_ok = smem_g <= size_t(max_optin);
-  const size_t attr = std::max(s_ok ? smem_s : 0, g_ok ? smem_g : 0);
-  if (attr > 0) SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attr)));
-  if (s_ok) SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, kern, kWPB * 32, smem_s));
-  if (g_ok) SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_g, kern, kWPB * 32, smem_g));
-  const bool keys_in_smem = per_s >= per_g && per_s > 0;
+  if (s_ok) {
+    SK_CUDA(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, kern_s, kWPB * 32, smem_s));
+  }
+  if (g_ok) {
+    SK_CUDA(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(std::max(smem_g, kern_g == kern_s && s_ok ? smem_s : size_t(0)))));
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_g, kern_g, kWPB * 32, smem_g));
+  }
+  const bool keys_in_smem = g_visited == SK_VISITED_SMEM      ? per_s > 0
+                            : g_visited == SK_VISITED_FINGERPRINT ? !(per_g > 0)
+                                                                : per_s >= per_g && per_s > 0;
   const int per_sm = keys_in_smem ? per_s : per_g;
   if (per_sm < 1) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM (smem " + std::to_string(smem_g) + ")");
   const sk::SmemLayout lay = keys_in_smem ? pl.lay_s : pl.lay_g;
@@ -154,15 +170,7 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   } else {
     pl.P.gkeys = nullptr;
   }
-  if constexpr (Eval::kSmemKeysVariant && !TRACE) {
-    if (keys_in_smem) {  // compile-time shared-memory probes for the production kernels
-      auto kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 1>;
-      SK_CUDA(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      kern_s<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
-      SK_CUDA(cudaGetLastError());
-      return SK_OK;
-    }
-  }
+  const KernT kern = keys_in_smem ? kern_s : kern_g;
   SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
   SK_CUDA(cudaGetLastError());
@@ -331,6 +339,13 @@ int sk_set_variant(int v) {
   return SK_OK;
 }
 int sk_get_variant(void) { return g_variant; }
+
+int sk_set_visited_layout(int mode) {
+  if (mode != SK_VISITED_AUTO && mode != SK_VISITED_SMEM && mode != SK_VISITED_FINGERPRINT)
+    return fail(SK_ERR_ARG, "unknown visited-set layout " + std::to_string(mode));
+  g_visited = mode;
+  return SK_OK;
+}
 
 int sk_saw_batch(int L, int n, const uint64_t* d_seeds, uint64_t master_seed, uint64_t batch, uint64_t walker_begin,
                  int64_t W, int64_t* d_best_e, uint64_t* d_best_words, int64_t* d_steps, uint8_t* d_dead,

@@ -130,14 +130,19 @@ __device__ __forceinline__ int32_t cand_delta(uint32_t key) { return (int32_t(ke
 // Per-walk visited set (_kernels.py:168-186 semantics: exact membership of
 // 64-bit keys).  Open addressing with linear probing, probed 32 slots at a
 // time by the whole warp: lane i inspects slot (start + i) & mask, a ballot
-// over the occupancy bitmap finds the end of the probe run, a second ballot
-// finds a key match inside the run.  Membership -- the only thing the walk
-// observes -- is identical to the reference's table whatever the capacity.
-// Occupancy lives in a bitmap so that key 0 is a legal key (no sentinel).
+// finds the end of the probe run, a second ballot finds a key match inside
+// the run.  Membership -- the only thing the walk observes -- is identical to
+// the reference's table whatever the capacity.  Two layouts:
+//   * keys in shared memory (KS = 1) with an occupancy bitmap, so that key 0
+//     is a legal key (no sentinel);
+//   * fingerprints (KS = 2): a nonzero 32-bit fingerprint per slot in shared
+//     memory (0 = empty) and the full keys in an L2-resident global scratch,
+//     read only when a fingerprint matches.  Half the shared memory per walk.
+// KS = 0 decides between the two at run time (keys_s != 0: keys in smem).
 // ---------------------------------------------------------------------------
 struct VisitedSet {
-  uint64_t* keys;  // [cap]  (stores u, see KeyState)
-  uint32_t* occ;   // [cap/32] occupancy bits
+  uint64_t* keys;  // [cap]  (stores u, see KeyState): smem, or global in fingerprint mode
+  uint32_t* occ;   // smem: [cap/32] occupancy bits, or [cap] fingerprints (0 = empty)
   uint32_t mask;   // cap - 1, cap a power of two >= 32
   uint32_t shift;  // 32 - log2(cap)
   uint32_t keys_s = 0;  // shared-window address of keys when they live in shared memory, else 0
@@ -145,19 +150,19 @@ struct VisitedSet {
   __device__ __forceinline__ void bind_shared() {
     keys_s = __isShared(keys) ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
   }
-  // KS = 1: keys are known (at compile time) to live in shared memory.
   template <int KS>
-  __device__ __forceinline__ uint64_t load_key(uint32_t slot) const {
-    if (KS == 1 || keys_s) {  // explicit LDS: generic loads of shared data cost extra latency on the probe path
-      uint64_t v;
-      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(keys_s + slot * 8u));
-      return v;
-    }
-    return keys[slot];
+  __device__ __forceinline__ bool smem_keys() const { return KS == 1 || (KS == 0 && keys_s != 0u); }
+
+  __device__ __forceinline__ uint64_t lds_key(uint32_t slot) const {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(keys_s + slot * 8u));
+    return v;
   }
 
+  template <int KS = 0>
   __device__ __forceinline__ void clear(int lane) {
-    for (uint32_t i = lane; i <= (mask >> 5); i += 32) occ[i] = 0u;
+    const uint32_t words = smem_keys<KS>() ? (mask >> 5) + 1u : mask + 1u;
+    for (uint32_t i = lane; i < words; i += 32) occ[i] = 0u;
   }
 
   __device__ __forceinline__ static uint32_t home(uint64_t u, uint32_t shift) {
@@ -165,33 +170,57 @@ struct VisitedSet {
     // for D <= 64, where it is KEY_SEED ^ words)
     return ((uint32_t(u) ^ uint32_t(u >> 32)) * 0x9E3779B1u) >> shift;
   }
+  __device__ __forceinline__ static uint32_t fingerprint(uint64_t u) {
+    return ((uint32_t(u >> 32) * 0x85EBCA6Bu) ^ uint32_t(u)) | 1u;  // never 0 (= empty)
+  }
 
   // Warp-collective.  Returns true iff u is present.  If absent and
   // `insert_if_absent`, the lane at the first free slot writes it.
   template <int KS = 0>
   __device__ __forceinline__ bool probe(uint64_t key, int lane, bool insert_if_absent) {
     uint32_t start = home(key, shift);
+    if (smem_keys<KS>()) {
+      for (;;) {
+        const uint32_t slot = (start + lane) & mask;
+        const uint32_t ow = occ[slot >> 5];
+        // load the slot's key alongside its occupancy word (stale keys of
+        // free slots are masked by `run` below)
+        const uint64_t kv = lds_key(slot);
+        const bool used = (ow >> (slot & 31)) & 1u;
+        const uint32_t empty_mask = __ballot_sync(kFull, !used);
+        // lanes strictly before the first empty slot are the live probe run
+        const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
+        const bool hit = ((run >> lane) & 1u) && kv == key;
+        if (__any_sync(kFull, hit)) return true;
+        if (empty_mask) {
+          if (insert_if_absent) {
+            const int first = __ffs(empty_mask) - 1;
+            if (lane == first) {
+              asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys_s + slot * 8u), "l"(key) : "memory");
+              atomicOr(&occ[slot >> 5], 1u << (slot & 31));
+            }
+            __syncwarp();
+          }
+          return false;
+        }
+        start = (start + 32) & mask;
+      }
+    }
+    const uint32_t f = fingerprint(key);
     for (;;) {
       const uint32_t slot = (start + lane) & mask;
-      const uint32_t ow = occ[slot >> 5];
-      // shared-memory keys: load the slot's key alongside its occupancy word
-      // (stale keys of free slots are masked by `run` below)
-      const uint64_t kv = KS == 1 ? load_key<1>(slot) : 0ull;
-      const bool used = (ow >> (slot & 31)) & 1u;
-      const uint32_t empty_mask = __ballot_sync(kFull, !used);
-      // lanes strictly before the first empty slot are the live probe run
+      const uint32_t x = occ[slot];
+      const uint32_t empty_mask = __ballot_sync(kFull, x == 0u);
       const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
-      const bool hit = ((run >> lane) & 1u) && (KS == 1 ? kv == key : load_key<KS>(slot) == key);
+      // full keys are read (from L2) only where the fingerprint matches
+      const bool hit = ((run >> lane) & 1u) && x == f && keys[slot] == key;
       if (__any_sync(kFull, hit)) return true;
       if (empty_mask) {
         if (insert_if_absent) {
           const int first = __ffs(empty_mask) - 1;
           if (lane == first) {
-            if (KS == 1 || keys_s)
-              asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys_s + slot * 8u), "l"(key) : "memory");
-            else
-              keys[slot] = key;
-            atomicOr(&occ[slot >> 5], 1u << (slot & 31));
+            keys[slot] = key;
+            occ[slot] = f;
           }
           __syncwarp();
         }

@@ -81,8 +81,8 @@ struct SmemLayout {
     }
     s.off_dl = o;
     if (need_dl) o = align_up(o + 4u * uint32_t(D), 16);
-    s.off_occ = o;
-    o = align_up(o + 4u * (cap / 32u), 16);
+    s.off_occ = o;  // occupancy bitmap (keys in smem) or per-slot fingerprints (keys in global)
+    o = align_up(o + 4u * (keys_in_smem ? cap / 32u : cap), 16);
     o = align_up(o, 32);  // evaluator area 32-byte aligned (signal blocks are 32-byte units)
     s.off_ext = o;
     o = align_up(o + ext_bytes, 32);  // every warp's area starts 32-byte aligned
@@ -158,7 +158,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   // ---- visited set with P1 (_kernels.py:220-226) ------------------------
   VisitedSet vs{sm.keys, sm.occ, P.cap - 1u, uint32_t(__clz(P.cap) + 1)};
   vs.bind_shared();
-  vs.clear(lane);
+  vs.clear<KS>(lane);
   __syncwarp();
   KeyState<NW> ks;
   ks.init(words);

@@ -29,12 +29,22 @@ from paper_2210_15962_b200.saw import WalkConfig, run_walk, run_walk_traced, wor
 VARIANTS = [_lib.VARIANT_SCALAR, _lib.VARIANT_FAST]
 
 
-@pytest.fixture(params=VARIANTS, ids=["scalar", "fast"])
+# (evaluator, visited-set layout): both evaluators, and the production
+# evaluator with the fingerprint layout forced (AUTO picks shared-memory keys
+# for most lengths)
+SETUPS = [(_lib.VARIANT_SCALAR, _lib.VISITED_AUTO), (_lib.VARIANT_FAST, _lib.VISITED_AUTO),
+          (_lib.VARIANT_FAST, _lib.VISITED_FINGERPRINT)]
+
+
+@pytest.fixture(params=SETUPS, ids=["scalar", "fast", "fast_fp"])
 def variant(request):
     old = _lib.get_variant()
-    _lib.set_variant(request.param)
-    yield request.param
+    ev, layout = request.param
+    _lib.set_variant(ev)
+    _lib.set_visited_layout(layout)
+    yield ev
     _lib.set_variant(old)
+    _lib.set_visited_layout(_lib.VISITED_AUTO)
 
 
 def sha(arr):
