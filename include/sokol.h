@@ -62,12 +62,14 @@ int sk_get_variant(void);
  * Visited-set layout of subsequent walk launches (process-global).  AUTO
  * picks by occupancy; SMEM keeps the 64-bit keys in shared memory;
  * FINGERPRINT keeps 32-bit fingerprints in shared memory and the keys in an
- * L2-resident global scratch (half the shared memory per walk).  Membership,
- * and so every result, is identical in all three.
+ * L2-resident global scratch; GLOBAL keeps only an occupancy bitmap in shared
+ * memory and the keys in the scratch.  Membership, and so every result, is
+ * identical in all of them.
  */
 #define SK_VISITED_AUTO 0
 #define SK_VISITED_SMEM 1
 #define SK_VISITED_FINGERPRINT 2
+#define SK_VISITED_GLOBAL 3
 int sk_set_visited_layout(int mode);
 
 /*

@@ -32,6 +32,7 @@ VARIANT_FAST = 2
 VISITED_AUTO = 0
 VISITED_SMEM = 1
 VISITED_FINGERPRINT = 2
+VISITED_GLOBAL = 3
 
 # Every symbol include/sokol.h declares; tests/test_abi.py checks the export
 # table against this list and against the header itself.

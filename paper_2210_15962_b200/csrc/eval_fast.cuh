@@ -141,7 +141,7 @@ struct EvalFast {
   static uint32_t ext_bytes(int L, int) { return fast_geom(L).ext_halves * 2u; }
   static bool supports(int L) { return L >= 3 && L <= SK_MAX_L; }
   static constexpr bool kNeedsDl = false;
-  static constexpr bool kSmemKeysVariant = (MT == 1);  // L <= 255: also built with compile-time smem probes
+  static constexpr bool kSmemKeysVariant = (MT <= 2);  // L <= 511: built per visited-set layout (compile-time probes)
   static constexpr bool kCeAliasKeys = true;  // C lives in registers + ces16 after init
   static constexpr int kMinBlocks = MT == 1 ? SK_MT1_MIN_BLOCKS : (MT == 2 ? SK_MT2_MIN_BLOCKS : 2);  // register caps chosen by measurement
   // Spin-array margins.  The C update reads s_{p -+ 2j} for every lag slot

@@ -94,8 +94,7 @@ constexpr uint32_t kSmemKeysMax = 32768;  // keys in smem up to 32 KB per walk
 
 struct Plan {
   sk::WalkParams P;
-  sk::SmemLayout lay_s;  // visited keys in shared memory
-  sk::SmemLayout lay_g;  // visited keys in an L2-resident global scratch
+  sk::SmemLayout lay[4];  // per visited-set layout (SK_VISITED_SMEM / _FINGERPRINT / _GLOBAL)
   bool smem_keys_ok;
   int nw;
   bool dry_run = false;  // compute the launch geometry only
@@ -113,56 +112,55 @@ Plan make_plan(int L, int n) {
   pl.P.K = D - 1;
   pl.P.cap = visited_capacity(n);
   pl.smem_keys_ok = pl.P.cap * 8u <= kSmemKeysMax;
-  pl.lay_s = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, true, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                  Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
-  pl.lay_g = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, false, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                  Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
+  for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++)
+    pl.lay[v] = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, v, Eval::ext_bytes(L, D), Eval::kNeedsDl,
+                                     Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
   return pl;
 }
 
-// Occupancy-driven placement of the visited keys: full keys in shared memory,
-// or fingerprints in shared memory with the keys in an L2-resident global
-// scratch, whichever lets more walks be resident (ties: shared memory).  The
-// production kernels (Eval::kSmemKeysVariant, no trace) are compiled for each
-// layout (KS = 1 / 2); the others decide at run time (KS = 0).
+// Occupancy-driven placement of the visited set: keys in shared memory, or
+// keys in an L2-resident global scratch with fingerprints or an occupancy
+// bitmap in shared memory -- whichever lets the most walks be resident (ties:
+// fingerprints, then shared-memory keys; measured).  The production kernels
+// (Eval::kSmemKeysVariant, no trace) are compiled per layout (KS = 1 / 2 / 3);
+// the others decide at run time (KS = 0).
 template <int NW, bool TRACE, class Eval>
 int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   using KernT = void (*)(sk::WalkParams, sk::SmemLayout);
-  KernT kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 0>;
-  KernT kern_g = kern_s;
+  KernT kern[4] = {nullptr, sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 0>, nullptr, nullptr};
+  kern[2] = kern[3] = kern[1];
   if constexpr (Eval::kSmemKeysVariant && !TRACE) {
-    kern_s = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 1>;
-    kern_g = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 2>;
+    kern[1] = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 1>;
+    kern[2] = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 2>;
+    kern[3] = sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 3>;
   }
-  int sms = 0, per_s = 0, per_g = 0;
+  int sms = 0, max_optin = 0, per[4] = {0, 0, 0, 0};
   SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t smem_s = size_t(pl.lay_s.total) * kWPB, smem_g = size_t(pl.lay_g.total) * kWPB;
-  int max_optin = 0;
   SK_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const bool s_ok = pl.smem_keys_ok && smem_s <= size_t(max_optin);
-  const bool g_ok = smem_g <= size_t(max_optin);
-  if (s_ok) {
-    SK_CUDA(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, kern_s, kWPB * 32, smem_s));
+  for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++) {
+    const size_t smem = size_t(pl.lay[v].total) * kWPB;
+    if (smem > size_t(max_optin) || (v == SK_VISITED_SMEM && !pl.smem_keys_ok)) continue;
+    SK_CUDA(cudaFuncSetAttribute(kern[v], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[v], kern[v], kWPB * 32, smem));
   }
-  if (g_ok) {
-    SK_CUDA(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(std::max(smem_g, kern_g == kern_s && s_ok ? smem_s : size_t(0)))));
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_g, kern_g, kWPB * 32, smem_g));
+  int mode = 0;
+  if (g_visited != SK_VISITED_AUTO && per[g_visited] > 0) {
+    mode = g_visited;
+  } else {
+    for (int v : {SK_VISITED_FINGERPRINT, SK_VISITED_SMEM, SK_VISITED_GLOBAL})
+      if (per[v] > 0 && (mode == 0 || per[v] > per[mode])) mode = v;
   }
-  const bool keys_in_smem = g_visited == SK_VISITED_SMEM      ? per_s > 0
-                            : g_visited == SK_VISITED_FINGERPRINT ? !(per_g > 0)
-                                                                : per_s >= per_g && per_s > 0;
-  const int per_sm = keys_in_smem ? per_s : per_g;
-  if (per_sm < 1) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM (smem " + std::to_string(smem_g) + ")");
-  const sk::SmemLayout lay = keys_in_smem ? pl.lay_s : pl.lay_g;
+  if (mode == 0) return fail(SK_ERR_UNSUPPORTED, "walk state does not fit one SM");
+  const int per_sm = per[mode];
+  const sk::SmemLayout lay = pl.lay[mode];
   pl.P.warp_smem = lay.total;
+  pl.P.visited_global_bitmap = mode == SK_VISITED_GLOBAL ? 1 : 0;
   const size_t smem = size_t(lay.total) * kWPB;
   const int64_t want = (pl.P.W + kWPB - 1) / kWPB;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms));
   pl.resident = int64_t(per_sm) * sms * kWPB;
   if (pl.dry_run) return SK_OK;
-  if (!keys_in_smem) {
+  if (mode != SK_VISITED_SMEM) {
     DevCache& c = cache_for(dev);
     int rc = grow(&c.gkeys, &c.gkeys_bytes, size_t(grid) * kWPB * pl.P.cap * 8u);
     if (rc) return rc;
@@ -170,9 +168,8 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   } else {
     pl.P.gkeys = nullptr;
   }
-  const KernT kern = keys_in_smem ? kern_s : kern_g;
-  SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
+  SK_CUDA(cudaFuncSetAttribute(kern[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern[mode]<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay);
   SK_CUDA(cudaGetLastError());
   return SK_OK;
 }
@@ -341,7 +338,8 @@ int sk_set_variant(int v) {
 int sk_get_variant(void) { return g_variant; }
 
 int sk_set_visited_layout(int mode) {
-  if (mode != SK_VISITED_AUTO && mode != SK_VISITED_SMEM && mode != SK_VISITED_FINGERPRINT)
+  if (mode != SK_VISITED_AUTO && mode != SK_VISITED_SMEM && mode != SK_VISITED_FINGERPRINT &&
+      mode != SK_VISITED_GLOBAL)
     return fail(SK_ERR_ARG, "unknown visited-set layout " + std::to_string(mode));
   g_visited = mode;
   return SK_OK;

@@ -137,8 +137,10 @@ __device__ __forceinline__ int32_t cand_delta(uint32_t key) { return (int32_t(ke
 //     is a legal key (no sentinel);
 //   * fingerprints (KS = 2): a nonzero 32-bit fingerprint per slot in shared
 //     memory (0 = empty) and the full keys in an L2-resident global scratch,
-//     read only when a fingerprint matches.  Half the shared memory per walk.
-// KS = 0 decides between the two at run time (keys_s != 0: keys in smem).
+//     read only when a fingerprint matches.  Half the shared memory per walk;
+//   * global keys (KS = 3): the occupancy bitmap in shared memory, the keys
+//     in the global scratch (read for the slots of the probe run).
+// KS = 0 decides at run time (keys_s != 0: keys in smem; else bitmap_global).
 // ---------------------------------------------------------------------------
 struct VisitedSet {
   uint64_t* keys;  // [cap]  (stores u, see KeyState): smem, or global in fingerprint mode
@@ -146,6 +148,7 @@ struct VisitedSet {
   uint32_t mask;   // cap - 1, cap a power of two >= 32
   uint32_t shift;  // 32 - log2(cap)
   uint32_t keys_s = 0;  // shared-window address of keys when they live in shared memory, else 0
+  bool bitmap_global = false;  // KS = 0 only: global keys with a bitmap (layout 3) instead of fingerprints
 
   __device__ __forceinline__ void bind_shared() {
     keys_s = __isShared(keys) ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
@@ -161,7 +164,8 @@ struct VisitedSet {
 
   template <int KS = 0>
   __device__ __forceinline__ void clear(int lane) {
-    const uint32_t words = smem_keys<KS>() ? (mask >> 5) + 1u : mask + 1u;
+    const bool bitmap = smem_keys<KS>() || KS == 3 || (KS == 0 && bitmap_global);
+    const uint32_t words = bitmap ? (mask >> 5) + 1u : mask + 1u;
     for (uint32_t i = lane; i < words; i += 32) occ[i] = 0u;
   }
 
@@ -197,6 +201,29 @@ struct VisitedSet {
             const int first = __ffs(empty_mask) - 1;
             if (lane == first) {
               asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys_s + slot * 8u), "l"(key) : "memory");
+              atomicOr(&occ[slot >> 5], 1u << (slot & 31));
+            }
+            __syncwarp();
+          }
+          return false;
+        }
+        start = (start + 32) & mask;
+      }
+    }
+    if (KS == 3 || (KS == 0 && bitmap_global)) {
+      // keys in global memory, occupancy bitmap in shared memory
+      for (;;) {
+        const uint32_t slot = (start + lane) & mask;
+        const bool used = (occ[slot >> 5] >> (slot & 31)) & 1u;
+        const uint32_t empty_mask = __ballot_sync(kFull, !used);
+        const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
+        const bool hit = ((run >> lane) & 1u) && keys[slot] == key;
+        if (__any_sync(kFull, hit)) return true;
+        if (empty_mask) {
+          if (insert_if_absent) {
+            const int first = __ffs(empty_mask) - 1;
+            if (lane == first) {
+              keys[slot] = key;
               atomicOr(&occ[slot >> 5], 1u << (slot & 31));
             }
             __syncwarp();

@@ -32,6 +32,7 @@ struct WalkParams {
   uint64_t* trace_words;    // TRACE only: [W][n+1][nw]
   int64_t* trace_deltas;    // TRACE only: [W][n][D]
   uint64_t* gkeys;          // global visited keys [nwarps][cap] or null (keys in smem)
+  int visited_global_bitmap;  // keys in global with an smem bitmap (SK_VISITED_GLOBAL), for KS = 0
   // multi-search mode (sk_saw_multi): W = R * W_rep walks; walk w belongs to
   // search r = w / W_rep with its own master seed and batch index, and
   // reduces into summary[r].  masters == nullptr: a single search.
@@ -61,12 +62,15 @@ struct SmemLayout {
   // span_hi: highest position index the evaluator reads (scalar: 2L-2, fast: L-1+K).
   // ce_alias_keys: the int32 C array is only read during init, so it may share
   // the visited-set key storage (cleared after init) when that is in smem.
-  __host__ __device__ static SmemLayout make(int L, int K, int D, uint32_t cap, bool keys_in_smem,
+  // visited: SK_VISITED_SMEM (keys + bitmap in smem), _FINGERPRINT (fingerprints
+  // in smem), _GLOBAL (bitmap in smem); keys live in global memory in the last two
+  __host__ __device__ static SmemLayout make(int L, int K, int D, uint32_t cap, int visited,
                                              uint32_t ext_bytes, bool need_dl, int span_hi, bool ce_alias_keys,
                                              int span_lo) {
     SmemLayout s;
     s.span_off = span_lo;  // zero cells below position 0 (>= L + 1, see the evaluators' span_lo)
     s.span = uint32_t(span_lo + span_hi + 1);
+    const bool keys_in_smem = visited == SK_VISITED_SMEM;
     const bool alias = ce_alias_keys && keys_in_smem && cap * 8u >= 4u * uint32_t(K + 1);
     uint32_t o = 0;
     s.off_keys = o;
@@ -82,7 +86,7 @@ struct SmemLayout {
     s.off_dl = o;
     if (need_dl) o = align_up(o + 4u * uint32_t(D), 16);
     s.off_occ = o;  // occupancy bitmap (keys in smem) or per-slot fingerprints (keys in global)
-    o = align_up(o + 4u * (keys_in_smem ? cap / 32u : cap), 16);
+    o = align_up(o + 4u * (visited == SK_VISITED_FINGERPRINT ? cap : cap / 32u), 16);
     o = align_up(o, 32);  // evaluator area 32-byte aligned (signal blocks are 32-byte units)
     s.off_ext = o;
     o = align_up(o + ext_bytes, 32);  // every warp's area starts 32-byte aligned
@@ -158,6 +162,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   // ---- visited set with P1 (_kernels.py:220-226) ------------------------
   VisitedSet vs{sm.keys, sm.occ, P.cap - 1u, uint32_t(__clz(P.cap) + 1)};
   vs.bind_shared();
+  vs.bitmap_global = P.visited_global_bitmap != 0;
   vs.clear<KS>(lane);
   __syncwarp();
   KeyState<NW> ks;

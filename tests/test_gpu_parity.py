@@ -30,13 +30,13 @@ VARIANTS = [_lib.VARIANT_SCALAR, _lib.VARIANT_FAST]
 
 
 # (evaluator, visited-set layout): both evaluators, and the production
-# evaluator with the fingerprint layout forced (AUTO picks shared-memory keys
+# evaluator with each global-key layout forced (AUTO picks shared-memory keys
 # for most lengths)
 SETUPS = [(_lib.VARIANT_SCALAR, _lib.VISITED_AUTO), (_lib.VARIANT_FAST, _lib.VISITED_AUTO),
-          (_lib.VARIANT_FAST, _lib.VISITED_FINGERPRINT)]
+          (_lib.VARIANT_FAST, _lib.VISITED_FINGERPRINT), (_lib.VARIANT_FAST, _lib.VISITED_GLOBAL)]
 
 
-@pytest.fixture(params=SETUPS, ids=["scalar", "fast", "fast_fp"])
+@pytest.fixture(params=SETUPS, ids=["scalar", "fast", "fast_fp", "fast_gk"])
 def variant(request):
     old = _lib.get_variant()
     ev, layout = request.param

@@ -31,6 +31,7 @@ def main():
 
     lib = _lib.load()
     _lib.set_variant(_lib.VARIANT_FAST if a.variant == "fast" else _lib.VARIANT_SCALAR)
+    _lib.set_visited_layout(int(os.environ.get("SK_SWEEP_LAYOUT", "0")))
     dev = torch.device("cuda", 0)
     summ = torch.empty(engine.SUMMARY_WORDS, dtype=torch.int64, device=dev)
     st = torch.cuda.current_stream()
