@@ -369,7 +369,8 @@ def load_ncu(L, W):
     with open(p) as f:
         d = json.load(f)
     out = {k: d[k] for k in ("source", "tensor_pipe_pct", "alu_pipe_pct", "lsu_pipe_pct", "issue_busy_pct",
-                             "warps_per_sm", "registers") if k in d}
+                             "warps_per_sm", "registers", "smem_wavefronts_pct", "smem_ld_bank_conflict_share")
+           if k in d}
     if d.get("L") == L and d.get("walks") and d.get("dram_bytes") is not None:
         out["traffic_bytes_per_launch"] = d["dram_bytes"] * (W / d["walks"])
         out["traffic_note"] = f"dram read+write of one captured launch ({d['walks']} walks), scaled to {W} walks"
