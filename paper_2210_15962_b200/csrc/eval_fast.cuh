@@ -80,10 +80,10 @@ __host__ __device__ inline FastGeom fast_geom(int L) {
   g.GLEN = (g.GLEN + 31) / 64 * 64 + 32;  // copy 2 sits 16 banks away from copy 1
   g.SPAD = 16 * (g.NB - 1) + 16;
   g.SLEN = g.SPAD + 16 * (g.NI + g.NB) + 32;
-  // S_1 starts 64 bytes (mod 128) after S_0: each half-warp of a B load reads
-  // two S_0 blocks and the same two S_1 blocks (column map below), side by
-  // side in the banks
-  g.SLEN = (g.SLEN + 63) / 64 * 64 + 32;
+  // S_1 starts 32 bytes (mod 128) after S_0: a half-warp of a B load reads
+  // S_0 blocks a, a+2 and S_1 blocks a, a+2 (column map below), which then
+  // fall on disjoint banks
+  g.SLEN = (g.SLEN + 63) / 64 * 64 + 16;
   // ... + ces (int16 C copy, D entries) + flip table (2 x D uint16 byte offsets)
   g.ext_halves = uint32_t(sig_off(g) + 2 * g.SLEN + ((D + 1) & ~1) + 2 * D);
   return g;
@@ -186,20 +186,23 @@ struct EvalFast {
     const int g = lane >> 2, t = lane & 3;
     const int x0 = 2 * t - g + 16 * G.MLO;
     a_addr = uint32_t(__cvta_generic_to_shared((g & 1) ? gb + G.GOFF + 1 + x0 : ga + G.GOFF + x0));
-    // Column map: column c holds parity pi = (c >> 1) & 1 and output block
-    // a = 2 (c >> 2) + (c & 1).  A lane's accumulator columns 2t, 2t+1 then
-    // share the parity t & 1, so the R update needs no per-slot parity test.
+    // Column map: column c of tile nt holds parity pi = (c >> 1) & 1 and
+    // output block a = 4 nt + ((c & 7) >> 2) + 2 (c & 1).  A lane's
+    // accumulator columns 2t, 2t+1 then share the parity t & 1, so the R
+    // update needs no per-slot parity test; and the lanes with t >> 1 = 0, 1
+    // sit one block (16 neighbours) apart, so the epilogue's and the R
+    // update's scattered spin / C loads avoid bank conflicts.
     lpar = t & 1;
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) {
       const int c = 8 * nt + g;
-      const int pi = (c >> 1) & 1, a = 2 * (c >> 2) + (c & 1);
+      const int pi = (c >> 1) & 1, a = 4 * nt + ((c & 7) >> 2) + 2 * (c & 1);
       const __half* sb = pi == 1 ? sp1 : sp0;  // columns with a >= NB are padding: any signal will do
       b_addr[nt] = uint32_t(__cvta_generic_to_shared(sb + G.SPAD + (a < G.NB ? 16 * (a + G.MLO) : 0) + 4 * t));
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int cc = 8 * nt + 2 * t + (o & 1);
-        const int ppi = (cc >> 1) & 1, aa = 2 * (cc >> 2) + (cc & 1);
+        const int ppi = (cc >> 1) & 1, aa = 4 * nt + ((cc & 7) >> 2) + 2 * (cc & 1);
         const int hp = 16 * aa + g + 8 * (o >> 1);
         const int h = 2 * hp + ppi;
         const bool ok = nt < G.NT && aa < G.NB && h < D;
