@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -51,7 +52,11 @@ struct DevCache {
   void* h_out = nullptr;
   size_t h_out_bytes = 0;
 };
-std::vector<DevCache> g_cache;
+// Scratch is cached per (device, stream): launches on different streams of one
+// device may run concurrently (engine.BatchEngine with several slices on one
+// device), so they must not share visited-key or word scratch.
+std::map<std::pair<int, uintptr_t>, DevCache> g_cache;
+std::mutex g_host_mu;  // serialises the synchronous host-buffer entry points
 
 int grow(void** p, size_t* have, size_t need) {
   if (*have >= need) return SK_OK;
@@ -67,9 +72,8 @@ int grow(void** p, size_t* have, size_t need) {
   return SK_OK;
 }
 
-DevCache& cache_for(int dev) {
-  if (int(g_cache.size()) <= dev) g_cache.resize(dev + 1);
-  return g_cache[dev];
+DevCache& cache_for(int dev, cudaStream_t st) {
+  return g_cache[std::make_pair(dev, reinterpret_cast<uintptr_t>(st))];
 }
 
 int validate(int L, int n, int64_t W) {
@@ -161,7 +165,7 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   pl.resident = int64_t(per_sm) * sms * kWPB;
   if (pl.dry_run) return SK_OK;
   if (mode != SK_VISITED_SMEM) {
-    DevCache& c = cache_for(dev);
+    DevCache& c = cache_for(dev, st);
     int rc = grow(&c.gkeys, &c.gkeys_bytes, size_t(grid) * kWPB * pl.P.cap * 8u);
     if (rc) return rc;
     pl.P.gkeys = static_cast<uint64_t*>(c.gkeys);
@@ -258,7 +262,7 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
   pl.P.batches = batches;
   pl.P.W_rep = W_rep;
   if (summary && !best_words && W > 0) {
-    DevCache& c = cache_for(dev);
+    DevCache& c = cache_for(dev, st);
     rc = grow(&c.words, &c.words_bytes, size_t(W) * pl.nw * 8u);
     if (rc) return rc;
     pl.P.best_words = static_cast<uint64_t*>(c.words);
@@ -381,9 +385,10 @@ int sk_saw_batch_host(int L, int n, const uint64_t* seeds, int64_t W, int64_t* b
   const size_t o_e = 0, o_w = o_e + size_t(W) * 8, o_s = o_w + size_t(W) * nw * 8, o_d = o_s + size_t(W) * 8;
   const size_t out_b = o_d + size_t(W);
   char *din, *dout;
+  std::lock_guard<std::mutex> hlk(g_host_mu);  // staging buffers are reused: one host call at a time
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    DevCache& c = cache_for(dev);
+    DevCache& c = cache_for(dev, nullptr);
     rc = grow(&c.h_in, &c.h_in_bytes, in_b);
     if (rc) return rc;
     rc = grow(&c.h_out, &c.h_out_bytes, out_b);
@@ -547,16 +552,16 @@ int sk_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   int cur = 0;
   cudaGetDevice(&cur);
-  for (size_t d = 0; d < g_cache.size(); d++) {
-    DevCache& c = g_cache[d];
+  for (auto& kv : g_cache) {
+    DevCache& c = kv.second;
     if (!c.gkeys && !c.words && !c.h_in && !c.h_out) continue;
-    cudaSetDevice(int(d));
+    cudaSetDevice(kv.first.first);
     if (c.gkeys) cudaFree(c.gkeys);
     if (c.words) cudaFree(c.words);
     if (c.h_in) cudaFree(c.h_in);
     if (c.h_out) cudaFree(c.h_out);
-    c = DevCache{};
   }
+  g_cache.clear();
   cudaSetDevice(cur);
   return SK_OK;
 }

@@ -59,18 +59,25 @@ def test_multi_equals_single_searches(L, W, R):
         np.testing.assert_array_equal(got[r], want, err_msg=f"search {r}")
 
 
-def test_run_multi_sharded_equals_run_batch():
-    L, W = 101, 96
+@pytest.mark.parametrize("layout", [_lib.VISITED_AUTO, _lib.VISITED_FINGERPRINT, _lib.VISITED_GLOBAL])
+def test_run_multi_sharded_equals_run_batch(layout):
+    # three shards on one device run on three streams, possibly concurrently:
+    # their global visited-key scratch must be private per stream
+    L, W = 101, 3 * 4096
     n = 8 * 51
     masters = [derive_repetition_seed(9, r) for r in range(6)]
     batches = [0, 3, 1, 7, 2, 2]
-    for devs in (None, [0, 0, 0]):  # three shards on one device exercise the merge
-        eng = engine.BatchEngine(L, W, n, 0, devices=devs)
-        res = eng.run_multi(masters, batches)
-        for m, b, x in zip(masters, batches, res):
-            y = engine.BatchEngine(L, W, n, m).run_batch(b)
-            assert (x.best_E, x.walker, x.steps_sum) == (y.best_E, y.walker, y.steps_sum)
-            np.testing.assert_array_equal(x.best_words, y.best_words)
+    _lib.set_visited_layout(layout)
+    try:
+        for devs in (None, [0, 0, 0]):
+            eng = engine.BatchEngine(L, W, n, 0, devices=devs)
+            res = eng.run_multi(masters, batches)
+            for m, b, x in zip(masters, batches, res):
+                y = engine.BatchEngine(L, W, n, m).run_batch(b)
+                assert (x.best_E, x.walker, x.steps_sum) == (y.best_E, y.walker, y.steps_sum)
+                np.testing.assert_array_equal(x.best_words, y.best_words)
+    finally:
+        _lib.set_visited_layout(_lib.VISITED_AUTO)
 
 
 def test_campaign_matches_reference_golden(golden_records):
