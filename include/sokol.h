@@ -14,6 +14,10 @@
  *          (equals the hex codec integer, codec.py:34-41).
  *   seeds: per-walk uint64 seeds as produced by derive_walk_seed
  *          (runner.py:53-57).
+ *
+ * Concurrency: device entry points are asynchronous on the given stream and
+ * may run concurrently on different streams (internal scratch is private per
+ * (device, stream)).  The *_host entry points are synchronous and serialised.
  */
 #ifndef SOKOL_H
 #define SOKOL_H
