@@ -239,9 +239,12 @@ struct VisitedSet {
       const uint32_t x = occ[slot];
       const uint32_t empty_mask = __ballot_sync(kFull, x == 0u);
       const uint32_t run = empty_mask ? ((empty_mask & (0u - empty_mask)) - 1u) : kFull;
-      // full keys are read (from L2) only where the fingerprint matches
-      const bool hit = ((run >> lane) & 1u) && x == f && keys[slot] == key;
-      if (__any_sync(kFull, hit)) return true;
+      // full keys are read (from L2) only where the fingerprint matches: a
+      // rare, warp-uniform branch (a true hit, or a fingerprint collision)
+      const bool fm = ((run >> lane) & 1u) && x == f;
+      if (__ballot_sync(kFull, fm)) {
+        if (__any_sync(kFull, fm && keys[slot] == key)) return true;
+      }
       if (empty_mask) {
         if (insert_if_absent) {
           const int first = __ffs(empty_mask) - 1;
