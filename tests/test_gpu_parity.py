@@ -129,6 +129,20 @@ def test_walk_factors_and_large_lengths_match_oracle(variant, oracle, L, factor)
         np.testing.assert_array_equal(g, x, err_msg=f"L={L} n={n}")
 
 
+@pytest.mark.parametrize("L", [223, 253, 255, 257, 259, 383, 385, 511, 513, 769])
+def test_tile_and_word_boundaries_match_oracle(variant, oracle, L):
+    # D = 128 / 129 (one -> two 8-column tiles), nw = 2 / 3 / 4 / 5 / 7 words,
+    # at the production walk factor 8
+    d = (L + 1) // 2
+    n = 8 * d
+    W = 8 if L > 500 else 16
+    seeds = oracle.derive_walk_seeds(4242, L, W)
+    got = gpu_batch(L, n, seeds)
+    want = oracle.batch_outputs(L, n, seeds)
+    for g, x, name in zip(got, want, ("best_e", "best_words", "steps", "dead")):
+        np.testing.assert_array_equal(g, x, err_msg=f"L={L} {name}")
+
+
 @pytest.mark.parametrize("L", [5, 9, 15, 21, 31, 47, 101, 149, 201])
 def test_traces_match_oracle(variant, oracle, L):
     d = (L + 1) // 2
