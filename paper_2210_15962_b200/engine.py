@@ -190,29 +190,30 @@ class BatchEngine:
         R = len(masters)
         if R != len(batches) or R < 1:
             raise ValueError("masters and batches must be non-empty and of equal length")
-        cache = self.__dict__.setdefault("_multi_cache", {})  # pinned/device buffers per search count
-        if R not in cache:
-            host_in = torch.empty((2, R), dtype=torch.int64, pin_memory=True)
-            per_dev = []
+        # pinned / device buffers, reused while they are large enough (capacity: a power of two)
+        if getattr(self, "_multi_cap", 0) < R:
+            cap = 1 << (R - 1).bit_length()
+            self._multi_cap = cap
+            self._multi_host = torch.empty(2 * cap, dtype=torch.int64, pin_memory=True)  # masters | batches
+            self._multi_dev = []
             for dev, _, _ in self.parts:
                 with torch.cuda.device(dev):
-                    per_dev.append((torch.empty((2, R), dtype=torch.int64, device=dev),
-                                    torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, device=dev),
-                                    torch.empty((R, SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)))
-            cache[R] = (host_in, per_dev)
-        host_in, per_dev = cache[R]
-        mb = host_in.numpy().view(np.uint64)
-        mb[0] = [int(m) & ((1 << 64) - 1) for m in masters]
-        mb[1] = [int(b) for b in batches]
+                    self._multi_dev.append((torch.empty(2 * cap, dtype=torch.int64, device=dev),
+                                            torch.empty((cap, SUMMARY_WORDS), dtype=torch.int64, device=dev),
+                                            torch.empty((cap, SUMMARY_WORDS), dtype=torch.int64, pin_memory=True)))
+        mb = self._multi_host.numpy().view(np.uint64)
+        mb[:R] = [int(m) & ((1 << 64) - 1) for m in masters]
+        mb[R:2 * R] = [int(b) for b in batches]
         outs = []
         for i, (dev, begin, cnt) in enumerate(self.parts):
-            d_in, summ, h = per_dev[i]
+            d_in, summ, h = self._multi_dev[i]
+            summ, h = summ[:R], h[:R]
             with torch.cuda.device(dev):
                 st = self.streams[i]
                 with torch.cuda.stream(st):
-                    d_in.copy_(host_in, non_blocking=True)
+                    d_in[:2 * R].copy_(self._multi_host[:2 * R], non_blocking=True)
                 _lib.check(self.lib.sk_saw_multi(
-                    self.L, self.n, d_in[0].data_ptr(), d_in[1].data_ptr(), R, int(begin), int(cnt),
+                    self.L, self.n, d_in.data_ptr(), d_in[R:].data_ptr(), R, int(begin), int(cnt),
                     summ.data_ptr(), st.cuda_stream,
                 ))
                 with torch.cuda.stream(st):
