@@ -253,12 +253,7 @@ struct EvalFast {
 #pragma unroll
     for (int nt = 0; nt < MT; nt++)
 #pragma unroll
-      for (int o = 0; o < 4; o++) {
-        // accA starts at 1.5 * 2^23: every partial sum stays an exact integer in
-        // [2^23, 2^24), so the float's bits are 0x4B400000 + X (no F2I needed)
-        accA[nt][o] = 12582912.0f;
-        accB[nt][o] = 0.f;
-      }
+      for (int o = 0; o < 4; o++) accA[nt][o] = accB[nt][o] = 0.f;
 
     // Y = sum_m A_m B_m; A pairs roll along m (pair x-8 of step m is pair x+8 of m-1).
     // The MMA count is padded to even; the extra block reads zero signal.
@@ -300,7 +295,7 @@ struct EvalFast {
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         const int h = hc[nt][o];
-        const int32_t X = __float_as_int(accA[nt][o] + accB[nt][o]) - 0x4B400000;
+        const int32_t X = __float2int_rn(accA[nt][o] + accB[nt][o]);
         const int32_t cx = cx0[-h];
         const int32_t sx = sx0[3 * h];
         const int32_t k = Rk[nt][o] - sx * sq2k[nt][o] - xsp64[nt][o] * X + xq64[nt][o] * cx;
