@@ -1,0 +1,9 @@
+#!/bin/bash
+# lambda(L) calibration on exact targets: campaigns of 100 concurrent repetitions at L=71..87,
+# each target the exact optimum from the device exhaustive scan; then the A/B of pending variants.
+set -x
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 1800 python tools/time_to_target.py --lengths 71,73,75,77,79,81,83,85,87 --reps 100 --exhaustive-max-d 44 > gpurun_out/calib_exact.jsonl 2> gpurun_out/calib_exact.err
+bash tools/gpu_ab.sh
+echo done

@@ -16,7 +16,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 name = sys.argv[1] if len(sys.argv) > 1 else "saw_walk_kernelILi2ELb0ENS_8EvalFastILi1ELi10EEELi4"
-lib = os.path.join(ROOT, "paper_2210_15962_b200", "libsokol.so")
+lib = os.environ.get("SOKOL_LIB") or os.path.join(ROOT, "paper_2210_15962_b200", "libsokol.so")
 with tempfile.TemporaryDirectory() as d:
     subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=d, capture_output=True)
     cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
