@@ -157,14 +157,15 @@ int64_t sk_resident_walks(int L, int n);
  * sk_exhaustive_scan: Gray indices g in [g_begin, g_begin + g_count) (the
  *   half after reference step g is gray(g) = g ^ (g >> 1); g = 0 is the
  *   all-plus start), asynchronous on `stream`.  Folds
- *   key = (E << 44) | g into *d_min_key with an atomic min, so the caller
+ *   key = (min(E, 2^17 - 1) << 47) | g into *d_min_key with an atomic min
+ *   (optima lie far below the saturation), so the caller
  *   initialises it to UINT64_MAX and may split the space into any slices;
  *   the final key's (E, g) is the reference's first minimum.
  * sk_exhaustive_scan_host: the whole space, synchronous; returns exactly the
  *   reference's (best_energy, best_bits), bit h of best_bits set iff half
  *   spin h is -1.
  */
-#define SK_MAX_EXHAUSTIVE_D 44
+#define SK_MAX_EXHAUSTIVE_D 47
 int sk_exhaustive_scan(int L, uint64_t g_begin, uint64_t g_count, uint64_t *d_min_key, void *stream);
 int sk_exhaustive_scan_host(int L, int64_t *best_e_out, int64_t *best_bits_out);
 

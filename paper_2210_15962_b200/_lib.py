@@ -23,7 +23,7 @@ SK_ERR_CUDA = -3
 SK_ERR_NOMEM = -4
 SK_MAX_L = 1023
 SK_MAX_WORDS = 8
-SK_MAX_EXHAUSTIVE_D = 44
+SK_MAX_EXHAUSTIVE_D = 47
 
 VARIANT_AUTO = 0
 VARIANT_SCALAR = 1

@@ -10,10 +10,11 @@
 // Here the g range is cut into chunks, one thread per chunk: the thread
 // rebuilds the state at its first g from scratch (O(L^2) with popcounts) and
 // then runs the same Gray sequence, h = ctz(g) for every g (valid for any
-// chunk start).  The result is the min over key = (E << 44) | g, i.e. the
-// lexicographic (E, g) minimum -- exactly the reference's first-minimum rule.
+// chunk start).  The result is the min over key = (E' << 47) | g with
+// E' = min(E, 2^17 - 1), i.e. the lexicographic (E, g) minimum -- exactly the
+// reference's first-minimum rule (the optimum lies far below the saturation).
 //
-// Per-thread state (D <= 44, so every parity class fits one uint64):
+// Per-thread state (D <= 47, so every parity class fits one uint64):
 //   P0 / P1  bit i set iff s_{2i} / s_{2i+1} == -1 (full skew sequence)
 //   cw[g]    C_{2j} + 128 as bytes, lags 4g+1..4g+4, in registers (G = ceil(K/4) groups)
 // A flip of half h negates positions p = h and q = L-1-h, which have the same
@@ -25,7 +26,8 @@
 
 namespace sk {
 
-constexpr int kExhKeyShift = 44;  // key = (E << 44) | g; g < 2^D <= 2^44, E < 2^20 for L <= 87
+constexpr int kExhKeyShift = 47;  // key = (E' << 47) | g; g < 2^D <= 2^47
+constexpr int32_t kExhEMax = (1 << 17) - 1;  // E' = min(E, kExhEMax)
 
 // Bits 4g..4g+3 of m, one per byte (bit i -> byte i): the four products
 // x * (1 + 2^7 + 2^14 + 2^21) land in disjoint bit ranges, so no carries.
@@ -34,8 +36,8 @@ __device__ __forceinline__ uint32_t spread4(uint64_t m, int g) {
   return (x * 0x00204081u) & 0x01010101u;
 }
 
-// One thread's chunk [g0, g1).  The even-lag correlations C_{2j} (|C| <= 85
-// for L <= 87) live as offset-binary bytes C + 128, four lags per register,
+// One thread's chunk [g0, g1).  The even-lag correlations C_{2j} (|C| <= 91
+// for L <= 93) live as offset-binary bytes C + 128, four lags per register,
 // so a move updates four lags with one add (the per-byte changes 8 n - 4 v
 // never carry or borrow across bytes) and E = sum C^2 is one signed
 // IDP4A per four lags after flipping the offset bit (x ^ 0x80 = C as int8).
@@ -130,7 +132,7 @@ __device__ __forceinline__ uint64_t exh_chunk(int L, uint64_t g0, uint64_t g1, c
       best_g = g;
     }
   }
-  return (uint64_t(uint32_t(best_e)) << kExhKeyShift) | best_g;
+  return (uint64_t(uint32_t(min(best_e, kExhEMax))) << kExhKeyShift) | best_g;
 }
 
 template <int G>

@@ -320,7 +320,8 @@ int exh_run(int L, uint64_t g_begin, uint64_t g_end, unsigned long long* key, cu
   if (G <= 8) return exh_launch<8>(L, g_begin, g_end, key, st, dev);
   if (G <= 9) return exh_launch<9>(L, g_begin, g_end, key, st, dev);
   if (G <= 10) return exh_launch<10>(L, g_begin, g_end, key, st, dev);
-  return exh_launch<11>(L, g_begin, g_end, key, st, dev);
+  if (G <= 11) return exh_launch<11>(L, g_begin, g_end, key, st, dev);
+  return exh_launch<12>(L, g_begin, g_end, key, st, dev);
 }
 
 __global__ void exh_key_init(unsigned long long* k) { *k = ~0ull; }
@@ -500,7 +501,7 @@ int sk_exhaustive_scan_host(int L, int64_t* best_e_out, int64_t* best_bits_out) 
   cudaStream_t st = 0;
   exh_key_init<<<1, 1, 0, st>>>(dkey);
   const int D = (L + 1) / 2;
-  const uint64_t total = 1ull << D, slice = 1ull << 36;  // bounded launches (~1 s each at D = 44)
+  const uint64_t total = 1ull << D, slice = 1ull << 36;  // bounded launches (~0.6 s each at D = 44)
   for (uint64_t b = 0; b < total && rc == SK_OK; b += slice) rc = exh_run(L, b, std::min(total, b + slice), dkey, st, dev);
   unsigned long long key = 0;
   if (rc == SK_OK && cudaMemcpy(&key, dkey, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -508,6 +509,8 @@ int sk_exhaustive_scan_host(int L, int64_t* best_e_out, int64_t* best_bits_out) 
   cudaFree(dkey);
   if (rc) return rc;
   const uint64_t g = key & ((1ull << sk::kExhKeyShift) - 1);
+  if (int64_t(key >> sk::kExhKeyShift) >= sk::kExhEMax)
+    return fail(SK_ERR_UNSUPPORTED, "minimum energy beyond the scan's key range");
   *best_e_out = int64_t(key >> sk::kExhKeyShift);
   *best_bits_out = int64_t(g ^ (g >> 1));
   return SK_OK;

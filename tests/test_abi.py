@@ -91,6 +91,6 @@ def test_exhaustive_scan_validation():
     be = np.zeros(1, np.int64)
     bb = np.zeros(1, np.int64)
     assert lib.sk_exhaustive_scan_host(4, be.ctypes.data, bb.ctypes.data) == _lib.SK_ERR_ARG
-    assert lib.sk_exhaustive_scan_host(89, be.ctypes.data, bb.ctypes.data) == _lib.SK_ERR_UNSUPPORTED
+    assert lib.sk_exhaustive_scan_host(95, be.ctypes.data, bb.ctypes.data) == _lib.SK_ERR_UNSUPPORTED
     assert lib.sk_exhaustive_scan_host(27, None, bb.ctypes.data) == _lib.SK_ERR_ARG
     assert lib.sk_exhaustive_scan(27, 1 << 14, 1, None, None) == _lib.SK_ERR_ARG

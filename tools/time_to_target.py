@@ -5,7 +5,7 @@ target campaigns.
     python tools/time_to_target.py --lengths 71,75,79,101,121 --reps 100
     python tools/time_to_target.py --direct 171,185 --direct-seeds 3 --max-runtime 900
 
-Targets per L: the exact optimum from the device exhaustive scan (L <= 87),
+Targets per L: the exact optimum from the device exhaustive scan (L <= 93),
 else the published best-known energy (L >= 171, published.py), else the best
 energy of a probe search (the reference's criterion-6 procedure,
 test_acceptance.py:140-160).  Each campaign runs `--reps` repetitions
