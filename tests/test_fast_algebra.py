@@ -134,3 +134,23 @@ def test_delta_is_multiple_of_8_and_fits_key(oracle):
             d = oracle.all_neighbor_deltas(L, s, c)
             assert np.all(d % 8 == 0)
             assert np.abs(d // 8).max() <= 8 * K + 2 * K * K < 2**20
+
+
+def test_packed_key_identity():
+    # the epilogue accumulates 64*dE + 2^29 + h directly; it must equal the
+    # packed selection key ((dE/8 + 2^20) << 9) | h for every reachable dE
+    # (multiples of 8, |dE/8| < 2^20) and h < 512, and order (dE, h) pairs
+    import random
+
+    rng = random.Random(5)
+    keys = []
+    for _ in range(20000):
+        d8 = rng.randint(-(1 << 20) + 1, (1 << 20) - 1)
+        h = rng.randint(0, 511)
+        dE = 8 * d8
+        a = (64 * dE + (1 << 29) + h) & 0xFFFFFFFF
+        b = ((d8 + (1 << 20)) << 9) | h
+        assert a == b
+        keys.append((a, dE, h))
+    keys.sort()
+    assert [(k[1], k[2]) for k in keys] == sorted((k[1], k[2]) for k in keys)
