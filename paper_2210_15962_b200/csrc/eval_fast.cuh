@@ -40,9 +40,6 @@
 #ifndef SK_MT1_MIN_BLOCKS
 #define SK_MT1_MIN_BLOCKS 4
 #endif
-#ifndef SK_MMA_CHAINS
-#define SK_MMA_CHAINS 2  // accumulator chains of the per-step MMA loop (experiment switch: 4)
-#endif
 #ifndef SK_MT2_MIN_BLOCKS
 #define SK_MT2_MIN_BLOCKS 3
 #endif
@@ -264,41 +261,17 @@ struct EvalFast {
 #pragma unroll
     for (int nt = 0; nt < MT; nt++) bb[nt] = b_addr[nt];
     uint32_t pm = lds32(aa - 16u);
-#if SK_MMA_CHAINS == 4
-    float accC[MT][4], accD[MT][4];
-#pragma unroll
-    for (int nt = 0; nt < MT; nt++)
-#pragma unroll
-      for (int o = 0; o < 4; o++) accC[nt][o] = accD[nt][o] = 0.f;
-#endif
     if (NMC > 0) {
 #pragma unroll
       for (int i = 0; i < NMC; i += 2) {
-#if SK_MMA_CHAINS == 4
-        // four accumulator chains: A/B on even pairs, C/D on odd pairs
-        mma_pair((i & 2) ? accC : accA, aa, bb, pm);
-#pragma unroll
-        for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
-        mma_pair((i & 2) ? accD : accB, aa + 32u, bb, pm);
-#else
         mma_pair(accA, aa, bb, pm);
 #pragma unroll
         for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
         mma_pair(accB, aa + 32u, bb, pm);
-#endif
         aa += 64u;
 #pragma unroll
         for (int nt = 0; nt < MT; nt++) bb[nt] += 32u;
       }
-#if SK_MMA_CHAINS == 4
-#pragma unroll
-      for (int nt = 0; nt < MT; nt++)
-#pragma unroll
-        for (int o = 0; o < 4; o++) {
-          accA[nt][o] += accC[nt][o];
-          accB[nt][o] += accD[nt][o];
-        }
-#endif
     } else {
       const int nm = G.MHI - G.MLO + 1;
       for (int i = 0; i < nm; i += 2) {
