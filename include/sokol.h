@@ -188,6 +188,23 @@ int sk_all_neighbor_deltas(int L, int64_t S, const int64_t *d_s, const int64_t *
                            void *stream);
 int sk_apply_neighbor(int L, int64_t S, int64_t *d_s, int64_t *d_c, const int64_t *d_h, void *stream);
 
+/*
+ * Evaluator probe: the walk kernels' own neighbourhood evaluator (the one
+ * sk_saw_batch selects for L under the current variant) run on S caller-given
+ * states instead of walk pivots.  Device memory, asynchronous on `stream`:
+ *   d_halves [S][D] int8 half sequences (+-1);
+ *   d_moves  [S][M] int32 half indices applied in order (M may be 0; an index
+ *            outside [0, D) leaves the state unchanged);
+ *   d_deltas [S][M+1][D] int64: row 0 = all_neighbor_deltas of the start
+ *            state (_kernels.py:162-165 over neighbor_delta, 85-123), row
+ *            i+1 = the same after apply_neighbor(moves[i]) (126-158).
+ * Exactly the rows the traced walk records (_kernels.py:241-243), for
+ * arbitrary (e.g. maximal-|C_k|) states; used to test the evaluator at its
+ * exactness bounds.
+ */
+int sk_eval_states(int L, int64_t S, const int8_t *d_halves, int M, const int32_t *d_moves, int64_t *d_deltas,
+                   void *stream);
+
 /* Release the library's cached device buffers (safe to call at any time). */
 int sk_shutdown(void);
 

@@ -203,6 +203,23 @@ def exhaustive_range(length: int, g_begin: int, g_count: int):
     return e, int(g[0])
 
 
+def exhaustive_scan_threaded(length: int, threads: int = 0, slices: int = 0):
+    """exhaustive_scan over all host threads: the Gray index range is cut
+    into slices scanned concurrently (ctypes releases the GIL); the first
+    minimum in Gray order is the minimum of the per-slice (E, g).  Returns
+    (E, bits) exactly as exhaustive_scan."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    threads = threads or num_procs()
+    total = 1 << ((length + 1) // 2)
+    k = slices or 4 * threads
+    cuts = [total * i // k for i in range(k + 1)]
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda ab: exhaustive_range(length, ab[0], ab[1] - ab[0]), zip(cuts, cuts[1:])))
+    e, g = min(parts)
+    return e, g ^ (g >> 1)
+
+
 def solve_record(L, walkers, walk_factor=8, master_seed=1, max_nses=None, target_E=None, threads: int = 0):
     """The reference's batch loop (runner.py:213-291) over the oracle's
     saw_batch; returns the RunRecord JSON dict minus wall_time_s.  Runtime

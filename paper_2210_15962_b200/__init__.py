@@ -9,7 +9,18 @@ there is no CPU execution path.
 """
 
 from .codec import DecodeError, decode, encode
-from .core import EnergyRecord, energy, expand_skew, half_dim, merit_factor
+from .core import (
+    EnergyRecord,
+    autocorrelation,
+    autocorrelations,
+    energy,
+    expand_skew,
+    half_dim,
+    merit_factor,
+    sidelobe_array,
+)
+from .neighborhood import EvalState, apply_flip, compute_deltas, flip, naive_oracle
+from .published import BEST_KNOWN, KnownResult
 from .runner import (
     RunConfig,
     RunRecord,
@@ -34,8 +45,9 @@ from .saw import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "DecodeError", "decode", "encode", "EnergyRecord", "energy", "expand_skew", "half_dim",
-    "merit_factor", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
+    "DecodeError", "decode", "encode", "EnergyRecord", "autocorrelation", "autocorrelations", "energy",
+    "expand_skew", "half_dim", "merit_factor", "sidelobe_array", "EvalState", "apply_flip", "compute_deltas",
+    "flip", "naive_oracle", "BEST_KNOWN", "KnownResult", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
     "derive_walk_seed", "solve", "target_campaign", "throughput_report", "WalkConfig",
     "WalkResult", "WalkTrace", "key", "run_walk", "run_walk_traced", "MAX_EXHAUSTIVE_D",
     "exhaustive_optimum",

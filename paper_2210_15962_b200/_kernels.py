@@ -11,6 +11,9 @@ reference's numba kernels, executed by libsokol.so on the current CUDA device:
         -> skewsaw._kernels.key_of_words (_kernels.py:46-53)
     exhaustive_scan(length) -> (best_e, best_bits)
         -> skewsaw._kernels.exhaustive_scan (_kernels.py:290-323)
+    eval_states(length, halves, moves) -> deltas [S, M+1, D]
+        the walk's evaluator on given states (all_neighbor_deltas +
+        apply_neighbor, _kernels.py:85-165), a test probe (sk_eval_states)
 
 Unlike numba, the C ABI validates its arguments and raises ``SokolError``
 (a RuntimeError) on bad input or a CUDA failure.
@@ -54,7 +57,7 @@ def _req(arr, dtype, name, shape=None):
 def saw_batch(length, n, seeds, best_e_out, best_words_out, steps_out, dead_out):
     """Run one independent walk per seed on the GPU; outputs written in place."""
     length = int(length)
-    n = int(n)
+    n = _lib.check_steps(n)
     d = (length + 1) // 2
     nw = (d + 63) // 64
     W = int(np.asarray(seeds).shape[0])
@@ -70,7 +73,7 @@ def saw_batch(length, n, seeds, best_e_out, best_words_out, steps_out, dead_out)
 def saw_walk(length, n, seed, best_words, trace_words, trace_deltas, record):
     """One walk; returns (best_e, steps, dead) like the reference."""
     length = int(length)
-    n = int(n)
+    n = _lib.check_steps(n)
     d = (length + 1) // 2
     nw = (d + 63) // 64
     p_bw = _req(best_words, np.uint64, "best_words", (nw,))
@@ -140,3 +143,33 @@ def apply_neighbor(s, c, h):
                                              torch.cuda.current_stream().cuda_stream))
     s[...] = ds.cpu().numpy()
     c[...] = dc.cpu().numpy()
+
+
+def eval_states(length, halves, moves=None):
+    """Delta vectors from the walk kernels' evaluator on given states.
+
+    halves: int8-convertible [S, D] of +-1; moves: int [S, M] half indices
+    (or None).  Returns int64 [S, M+1, D]: row 0 is the neighbourhood of the
+    start state, row i+1 the neighbourhood after applying moves[:, :i+1]
+    (apply_neighbor semantics, no visited check)."""
+    import torch
+
+    length = int(length)
+    d = (length + 1) // 2
+    h = np.ascontiguousarray(halves, dtype=np.int8)
+    if h.ndim != 2 or h.shape[1] != d or not np.all(np.abs(h) == 1):
+        raise ValueError(f"halves must be [S, {d}] of +-1")
+    S = h.shape[0]
+    mv = np.zeros((S, 0), np.int32) if moves is None else np.ascontiguousarray(moves, dtype=np.int32)
+    if mv.ndim != 2 or mv.shape[0] != S or (mv.size and (mv.min() < 0 or mv.max() >= d)):
+        raise ValueError(f"moves must be [S, M] half indices in [0, {d})")
+    M = mv.shape[1]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dh = torch.from_numpy(h).to(dev)
+    dm = torch.from_numpy(mv).to(dev) if M else None
+    out = torch.empty((S, M + 1, d), dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    _lib.check(_lib.load().sk_eval_states(length, S, dh.data_ptr(), M, dm.data_ptr() if M else None,
+                                          out.data_ptr(), st.cuda_stream))
+    st.synchronize()
+    return out.cpu().numpy()

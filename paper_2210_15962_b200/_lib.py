@@ -53,6 +53,7 @@ EXPORTS = (
     "sk_exhaustive_scan_host",
     "sk_all_neighbor_deltas",
     "sk_apply_neighbor",
+    "sk_eval_states",
     "sk_shutdown",
 )
 
@@ -116,6 +117,8 @@ def _declare(lib):
     lib.sk_all_neighbor_deltas.restype = _i
     lib.sk_apply_neighbor.argtypes = [_i, _i64, _vp, _vp, _vp, _vp]
     lib.sk_apply_neighbor.restype = _i
+    lib.sk_eval_states.argtypes = [_i, _i64, _vp, _i, _vp, _vp, _vp]
+    lib.sk_eval_states.restype = _i
     lib.sk_shutdown.restype = _i
 
 
@@ -140,6 +143,20 @@ def check(rc: int):
     if rc != SK_OK:
         msg = load().sk_last_error()
         raise SokolError(rc, msg.decode() if msg else "")
+
+
+INT32_MAX = (1 << 31) - 1
+
+
+def check_steps(n: int) -> int:
+    """The C ABI takes the walk step count as a C int; ctypes would truncate
+    a larger value silently, so it is rejected here (the reference accepts any
+    n >= 1, runner.py:81-97, but a walk of 2^31 steps needs a 2^35-byte
+    visited set per walk)."""
+    n = int(n)
+    if n > INT32_MAX:
+        raise SokolError(SK_ERR_UNSUPPORTED, f"walk step count n={n} exceeds the C ABI's int range")
+    return n
 
 
 def set_variant(variant: int):

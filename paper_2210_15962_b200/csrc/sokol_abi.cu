@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sokol.h"
@@ -51,6 +52,8 @@ struct DevCache {
   size_t h_in_bytes = 0;
   void* h_out = nullptr;
   size_t h_out_bytes = 0;
+  void* h_walk = nullptr;  // sk_saw_walk_host staging (seed, outputs, trace)
+  size_t h_walk_bytes = 0;
 };
 // Scratch is cached per (device, stream): launches on different streams of one
 // device may run concurrently (engine.BatchEngine with several slices on one
@@ -76,21 +79,25 @@ DevCache& cache_for(int dev, cudaStream_t st) {
   return g_cache[std::make_pair(dev, reinterpret_cast<uintptr_t>(st))];
 }
 
+constexpr uint64_t kMaxVisitedCap = uint64_t(1) << 30;  // keys scratch per resident walk <= 8 GiB
+
+uint64_t visited_capacity(int n) {
+  // strictly larger than the n+1 keys a walk can insert, load <= 15/16
+  const uint64_t need = std::max<uint64_t>(32, (uint64_t(n) + 1) * 16 / 15 + 1);
+  uint64_t cap = 32;
+  while (cap < need) cap <<= 1;
+  return cap;
+}
+
 int validate(int L, int n, int64_t W) {
   if (L < 3 || (L % 2) == 0) return fail(SK_ERR_ARG, "length must be odd and >= 3, got " + std::to_string(L));
   if (L > SK_MAX_L)
     return fail(SK_ERR_UNSUPPORTED, "length " + std::to_string(L) + " exceeds SK_MAX_L=" + std::to_string(SK_MAX_L));
   if (n < 1) return fail(SK_ERR_ARG, "walk step count n must be >= 1");
+  if (visited_capacity(n) > kMaxVisitedCap)
+    return fail(SK_ERR_UNSUPPORTED, "walk step count n=" + std::to_string(n) + " needs a visited set beyond 2^30 slots");
   if (W < 0) return fail(SK_ERR_ARG, "walker count must be >= 0");
   return SK_OK;
-}
-
-uint32_t visited_capacity(int n) {
-  // strictly larger than the n+1 keys a walk can insert, load <= 15/16
-  const uint64_t need = std::max<uint64_t>(32, (uint64_t(n) + 1) * 16 / 15 + 1);
-  uint32_t cap = 32;
-  while (cap < need) cap <<= 1;
-  return cap;
 }
 
 constexpr int kWPB = 4;                  // warps per block (one walk per warp)
@@ -114,7 +121,7 @@ Plan make_plan(int L, int n) {
   pl.P.n = n;
   pl.P.D = D;
   pl.P.K = D - 1;
-  pl.P.cap = visited_capacity(n);
+  pl.P.cap = uint32_t(visited_capacity(n));
   pl.smem_keys_ok = pl.P.cap * 8u <= kSmemKeysMax;
   for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++)
     pl.lay[v] = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, v, Eval::ext_bytes(L, D), Eval::kNeedsDl,
@@ -158,7 +165,7 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   const int per_sm = per[mode];
   const sk::SmemLayout lay = pl.lay[mode];
   pl.P.warp_smem = lay.total;
-  pl.P.visited_global_bitmap = mode == SK_VISITED_GLOBAL ? 1 : 0;
+  pl.P.visited_mode = mode;
   const size_t smem = size_t(lay.total) * kWPB;
   const int64_t want = (pl.P.W + kWPB - 1) / kWPB;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms));
@@ -178,51 +185,62 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   return SK_OK;
 }
 
-template <bool TRACE, class Eval>
-int launch_eval(Plan& pl, cudaStream_t st, int dev) {
-  switch (pl.nw) {
-    case 1: return launch_nw<1, TRACE, Eval>(pl, st, dev);
-    case 2: return launch_nw<2, TRACE, Eval>(pl, st, dev);
-    case 3: return launch_nw<3, TRACE, Eval>(pl, st, dev);
-    case 4: return launch_nw<4, TRACE, Eval>(pl, st, dev);
-    case 5: return launch_nw<5, TRACE, Eval>(pl, st, dev);
-    case 6: return launch_nw<6, TRACE, Eval>(pl, st, dev);
-    case 7: return launch_nw<7, TRACE, Eval>(pl, st, dev);
-    case 8: return launch_nw<8, TRACE, Eval>(pl, st, dev);
+// Evaluator dispatch: calls f(std::integral_constant<int, NW>, (Eval*)0) with
+// the word count and the evaluator the walk kernels use for this length
+// (scalar, or the production evaluator with a compile-time tile bound
+// MT = ceil(NW/2) and, for one tile, a compile-time MMA count).  Every
+// launch -- walks, traces, the evaluator probe -- goes through here, so the
+// probe runs exactly the instantiation the batch kernel runs.
+template <int NW, class F>
+int dispatch_fast_small(int L, F&& f) {
+  const sk::FastGeom g = sk::fast_geom(L);
+  const int nm = ((g.MHI - g.MLO + 1) + 1) & ~1;
+  using NWc = std::integral_constant<int, NW>;
+  switch (nm) {
+    case 2: return f(NWc{}, (sk::EvalFast<1, 2>*)nullptr);
+    case 4: return f(NWc{}, (sk::EvalFast<1, 4>*)nullptr);
+    case 6: return f(NWc{}, (sk::EvalFast<1, 6>*)nullptr);
+    case 8: return f(NWc{}, (sk::EvalFast<1, 8>*)nullptr);
+    case 10: return f(NWc{}, (sk::EvalFast<1, 10>*)nullptr);
+    case 12: return f(NWc{}, (sk::EvalFast<1, 12>*)nullptr);
   }
-  return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
+  return f(NWc{}, (sk::EvalFast<1, 0>*)nullptr);
 }
 
-template <int NW, bool TRACE>
-int launch_fast_small(Plan& pl, cudaStream_t st, int dev) {
-  // one 8-column tile (D <= 128): the per-step MMA count is a compile-time constant
-  const sk::FastGeom g = sk::fast_geom(pl.P.L);
-  const int nm = ((g.MHI - g.MLO + 1) + 1) & ~1;
-  switch (nm) {
-    case 2: return launch_nw<NW, TRACE, sk::EvalFast<1, 2>>(pl, st, dev);
-    case 4: return launch_nw<NW, TRACE, sk::EvalFast<1, 4>>(pl, st, dev);
-    case 6: return launch_nw<NW, TRACE, sk::EvalFast<1, 6>>(pl, st, dev);
-    case 8: return launch_nw<NW, TRACE, sk::EvalFast<1, 8>>(pl, st, dev);
-    case 10: return launch_nw<NW, TRACE, sk::EvalFast<1, 10>>(pl, st, dev);
-    case 12: return launch_nw<NW, TRACE, sk::EvalFast<1, 12>>(pl, st, dev);
+template <class F>
+int dispatch_eval(int L, int nw, bool scalar, F&& f) {
+  if (scalar) {
+    switch (nw) {
+      case 1: return f(std::integral_constant<int, 1>{}, (sk::EvalScalar*)nullptr);
+      case 2: return f(std::integral_constant<int, 2>{}, (sk::EvalScalar*)nullptr);
+      case 3: return f(std::integral_constant<int, 3>{}, (sk::EvalScalar*)nullptr);
+      case 4: return f(std::integral_constant<int, 4>{}, (sk::EvalScalar*)nullptr);
+      case 5: return f(std::integral_constant<int, 5>{}, (sk::EvalScalar*)nullptr);
+      case 6: return f(std::integral_constant<int, 6>{}, (sk::EvalScalar*)nullptr);
+      case 7: return f(std::integral_constant<int, 7>{}, (sk::EvalScalar*)nullptr);
+      case 8: return f(std::integral_constant<int, 8>{}, (sk::EvalScalar*)nullptr);
+    }
+    return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
   }
-  return launch_nw<NW, TRACE, sk::EvalFast<1, 0>>(pl, st, dev);
+  switch (nw) {
+    case 1: return dispatch_fast_small<1>(L, f);
+    case 2: return dispatch_fast_small<2>(L, f);
+    case 3: return f(std::integral_constant<int, 3>{}, (sk::EvalFast<2>*)nullptr);
+    case 4: return f(std::integral_constant<int, 4>{}, (sk::EvalFast<2>*)nullptr);
+    case 5: return f(std::integral_constant<int, 5>{}, (sk::EvalFast<3>*)nullptr);
+    case 6: return f(std::integral_constant<int, 6>{}, (sk::EvalFast<3>*)nullptr);
+    case 7: return f(std::integral_constant<int, 7>{}, (sk::EvalFast<4>*)nullptr);
+    case 8: return f(std::integral_constant<int, 8>{}, (sk::EvalFast<4>*)nullptr);
+  }
+  return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
 }
 
 template <bool TRACE>
-int launch_fast(Plan& pl, cudaStream_t st, int dev) {
-  // compile-time tile bound MT = ceil(NW/2) covers every L with that word count
-  switch (pl.nw) {
-    case 1: return launch_fast_small<1, TRACE>(pl, st, dev);
-    case 2: return launch_fast_small<2, TRACE>(pl, st, dev);
-    case 3: return launch_nw<3, TRACE, sk::EvalFast<2>>(pl, st, dev);
-    case 4: return launch_nw<4, TRACE, sk::EvalFast<2>>(pl, st, dev);
-    case 5: return launch_nw<5, TRACE, sk::EvalFast<3>>(pl, st, dev);
-    case 6: return launch_nw<6, TRACE, sk::EvalFast<3>>(pl, st, dev);
-    case 7: return launch_nw<7, TRACE, sk::EvalFast<4>>(pl, st, dev);
-    case 8: return launch_nw<8, TRACE, sk::EvalFast<4>>(pl, st, dev);
-  }
-  return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
+int launch_walks(Plan& pl, bool scalar, cudaStream_t st, int dev) {
+  return dispatch_eval(pl.P.L, pl.nw, scalar, [&](auto nwc, auto* evp) {
+    using Eval = std::remove_pointer_t<decltype(evp)>;
+    return launch_nw<decltype(nwc)::value, TRACE, Eval>(pl, st, dev);
+  });
 }
 
 // R > 0 with masters/batches: multi-search mode, W walks per search
@@ -272,7 +290,7 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
     SK_CUDA(cudaGetLastError());
   }
   if (W > 0) {
-    rc = scalar ? launch_eval<TRACE, sk::EvalScalar>(pl, st, dev) : launch_fast<TRACE>(pl, st, dev);
+    rc = launch_walks<TRACE>(pl, scalar, st, dev);
     if (rc) return rc;
   }
   if (summary && W > 0) {
@@ -419,15 +437,20 @@ int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t* best_words, uint64_t
   if (record && (!trace_words || !trace_deltas)) return fail(SK_ERR_ARG, "sk_saw_walk_host: record needs trace buffers");
   const int D = (L + 1) / 2, nw = (D + 63) / 64;
   const size_t tw_b = record ? size_t(n + 1) * nw * 8 : 0, td_b = record ? size_t(n) * D * 8 : 0;
-  char* buf = nullptr;
   const size_t o_seed = 0, o_e = 8, o_s = 16, o_d = 24, o_w = 32, o_tw = o_w + size_t(nw) * 8, o_td = o_tw + tw_b;
-  SK_CUDA(cudaMalloc(&buf, o_td + td_b));
-  cudaStream_t st = 0;
-  auto cleanup = [&]() { cudaFree(buf); };
-  if (cudaMemcpyAsync(buf + o_seed, &seed, 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-    cleanup();
-    return fail(SK_ERR_CUDA, "seed copy failed");
+  std::lock_guard<std::mutex> hlk(g_host_mu);  // the staging buffer is reused: one host call at a time
+  char* buf = nullptr;
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCache& c = cache_for(dev, nullptr);
+    rc = grow(&c.h_walk, &c.h_walk_bytes, o_td + td_b);  // cached: no cudaMalloc per replayed walk
+    if (rc) return rc;
+    buf = static_cast<char*>(c.h_walk);
   }
+  cudaStream_t st = 0;
+  SK_CUDA(cudaMemcpyAsync(buf + o_seed, &seed, 8, cudaMemcpyHostToDevice, st));
   if (record) {
     rc = run<true>(L, n, reinterpret_cast<uint64_t*>(buf + o_seed), 0, 0, 0, 1, reinterpret_cast<int64_t*>(buf + o_e),
                    reinterpret_cast<uint64_t*>(buf + o_w), reinterpret_cast<int64_t*>(buf + o_s),
@@ -438,27 +461,20 @@ int sk_saw_walk_host(int L, int n, uint64_t seed, uint64_t* best_words, uint64_t
                     reinterpret_cast<uint64_t*>(buf + o_w), reinterpret_cast<int64_t*>(buf + o_s),
                     reinterpret_cast<uint8_t*>(buf + o_d), nullptr, nullptr, nullptr, st);
   }
-  if (rc) {
-    cleanup();
-    return rc;
-  }
-  bool ok = cudaMemcpyAsync(best_e_out, buf + o_e, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-            cudaMemcpyAsync(steps_out, buf + o_s, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-            cudaMemcpyAsync(dead_out, buf + o_d, 1, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-            cudaMemcpyAsync(best_words, buf + o_w, size_t(nw) * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess;
-  if (ok && record) {
+  if (rc) return rc;
+  SK_CUDA(cudaMemcpyAsync(best_e_out, buf + o_e, 8, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(steps_out, buf + o_s, 8, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(dead_out, buf + o_d, 1, cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaMemcpyAsync(best_words, buf + o_w, size_t(nw) * 8, cudaMemcpyDeviceToHost, st));
+  if (record) {
     // rows past the walk's end are left untouched by the kernel: copy only
     // what was written so that caller-initialised rows survive (saw.py:108-110)
-    ok = cudaStreamSynchronize(st) == cudaSuccess;
-    if (ok) {
-      const int64_t rows_w = *steps_out + 1, rows_d = *steps_out + (*dead_out ? 1 : 0);
-      ok = cudaMemcpyAsync(trace_words, buf + o_tw, size_t(rows_w) * nw * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-           cudaMemcpyAsync(trace_deltas, buf + o_td, size_t(rows_d) * D * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess;
-    }
+    SK_CUDA(cudaStreamSynchronize(st));
+    const int64_t rows_w = *steps_out + 1, rows_d = *steps_out + (*dead_out ? 1 : 0);
+    SK_CUDA(cudaMemcpyAsync(trace_words, buf + o_tw, size_t(rows_w) * nw * 8, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaMemcpyAsync(trace_deltas, buf + o_td, size_t(rows_d) * D * 8, cudaMemcpyDeviceToHost, st));
   }
-  ok = ok && cudaStreamSynchronize(st) == cudaSuccess;
-  cleanup();
-  if (!ok) return fail(SK_ERR_CUDA, std::string("sk_saw_walk_host: ") + cudaGetErrorString(cudaGetLastError()));
+  SK_CUDA(cudaStreamSynchronize(st));
   return SK_OK;
 }
 
@@ -471,7 +487,7 @@ int64_t sk_resident_walks(int L, int n) {
   Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
   pl.P.W = int64_t(1) << 40;
   pl.dry_run = true;
-  const int rc = scalar ? launch_eval<false, sk::EvalScalar>(pl, 0, dev) : launch_fast<false>(pl, 0, dev);
+  const int rc = launch_walks<false>(pl, scalar, 0, dev);
   return rc ? -1 : pl.resident;
 }
 
@@ -551,18 +567,52 @@ int sk_apply_neighbor(int L, int64_t S, int64_t* d_s, int64_t* d_c, const int64_
   return SK_OK;
 }
 
+int sk_eval_states(int L, int64_t S, const int8_t* d_halves, int M, const int32_t* d_moves, int64_t* d_deltas,
+                   void* stream) {
+  int rc = validate(L, 1, S);
+  if (rc) return rc;
+  if (M < 0) return fail(SK_ERR_ARG, "move count must be >= 0");
+  if (S == 0) return SK_OK;
+  if (!d_halves || !d_deltas || (M > 0 && !d_moves)) return fail(SK_ERR_ARG, "sk_eval_states: null buffer");
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0, sms = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int D = (L + 1) / 2, nw = (D + 63) / 64;
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return dispatch_eval(L, nw, scalar, [&](auto nwc, auto* evp) {
+    using Eval = std::remove_pointer_t<decltype(evp)>;
+    Plan pl = make_plan<Eval>(L, 1);
+    const sk::SmemLayout lay = pl.lay[SK_VISITED_GLOBAL];  // no visited set: the smallest layout
+    pl.P.W = S;
+    pl.P.warp_smem = lay.total;
+    auto kern = sk::eval_states_kernel<decltype(nwc)::value, Eval, kWPB>;
+    const size_t smem = size_t(lay.total) * kWPB;
+    SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per = 0;
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kWPB * 32, smem));
+    if (per < 1) return fail(SK_ERR_UNSUPPORTED, "evaluator state does not fit one SM");
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((S + kWPB - 1) / kWPB, int64_t(per) * sms));
+    kern<<<dim3(unsigned(grid)), dim3(kWPB * 32), smem, st>>>(pl.P, lay, d_halves, M, d_moves, d_deltas);
+    SK_CUDA(cudaGetLastError());
+    return SK_OK;
+  });
+}
+
 int sk_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   int cur = 0;
   cudaGetDevice(&cur);
   for (auto& kv : g_cache) {
     DevCache& c = kv.second;
-    if (!c.gkeys && !c.words && !c.h_in && !c.h_out) continue;
+    if (!c.gkeys && !c.words && !c.h_in && !c.h_out && !c.h_walk) continue;
     cudaSetDevice(kv.first.first);
     if (c.gkeys) cudaFree(c.gkeys);
     if (c.words) cudaFree(c.words);
     if (c.h_in) cudaFree(c.h_in);
     if (c.h_out) cudaFree(c.h_out);
+    if (c.h_walk) cudaFree(c.h_walk);
   }
   g_cache.clear();
   cudaSetDevice(cur);

@@ -140,21 +140,26 @@ __device__ __forceinline__ int32_t cand_delta(uint32_t key) { return (int32_t(ke
 //     read only when a fingerprint matches.  Half the shared memory per walk;
 //   * global keys (KS = 3): the occupancy bitmap in shared memory, the keys
 //     in the global scratch (read for the slots of the probe run).
-// KS = 0 decides at run time (keys_s != 0: keys in smem; else bitmap_global).
+// KS = 0 decides at run time from the launch's layout (bind()).
 // ---------------------------------------------------------------------------
 struct VisitedSet {
   uint64_t* keys;  // [cap]  (stores u, see KeyState): smem, or global in fingerprint mode
   uint32_t* occ;   // smem: [cap/32] occupancy bits, or [cap] fingerprints (0 = empty)
   uint32_t mask;   // cap - 1, cap a power of two >= 32
   uint32_t shift;  // 32 - log2(cap)
-  uint32_t keys_s = 0;  // shared-window address of keys when they live in shared memory, else 0
+  uint32_t keys_s = 0;  // shared-window address of keys when they live in shared memory
+  bool keys_shared = false;    // KS = 0 only: the launch placed the keys in shared memory (layout 1)
   bool bitmap_global = false;  // KS = 0 only: global keys with a bitmap (layout 3) instead of fingerprints
 
-  __device__ __forceinline__ void bind_shared() {
-    keys_s = __isShared(keys) ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
+  // The layout is the launch's explicit choice (WalkParams::visited_mode), not
+  // inferred from the address, so a key array at shared offset 0 is fine.
+  __device__ __forceinline__ void bind(int visited_mode) {
+    keys_shared = visited_mode == SK_VISITED_SMEM;
+    bitmap_global = visited_mode == SK_VISITED_GLOBAL;
+    keys_s = keys_shared ? uint32_t(__cvta_generic_to_shared(keys)) : 0u;
   }
   template <int KS>
-  __device__ __forceinline__ bool smem_keys() const { return KS == 1 || (KS == 0 && keys_s != 0u); }
+  __device__ __forceinline__ bool smem_keys() const { return KS == 1 || (KS == 0 && keys_shared); }
 
   __device__ __forceinline__ uint64_t lds_key(uint32_t slot) const {
     uint64_t v;

@@ -32,7 +32,7 @@ struct WalkParams {
   uint64_t* trace_words;    // TRACE only: [W][n+1][nw]
   int64_t* trace_deltas;    // TRACE only: [W][n][D]
   uint64_t* gkeys;          // global visited keys [nwarps][cap] or null (keys in smem)
-  int visited_global_bitmap;  // keys in global with an smem bitmap (SK_VISITED_GLOBAL), for KS = 0
+  int visited_mode;         // SK_VISITED_SMEM / _FINGERPRINT / _GLOBAL chosen by the launch
   // multi-search mode (sk_saw_multi): W = R * W_rep walks; walk w belongs to
   // search r = w / W_rep with its own master seed and batch index, and
   // reduces into summary[r].  masters == nullptr: a single search.
@@ -161,8 +161,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
 
   // ---- visited set with P1 (_kernels.py:220-226) ------------------------
   VisitedSet vs{sm.keys, sm.occ, P.cap - 1u, uint32_t(__clz(P.cap) + 1)};
-  vs.bind_shared();
-  vs.bitmap_global = P.visited_global_bitmap != 0;
+  vs.bind(P.visited_mode);
   vs.clear<KS>(lane);
   __syncwarp();
   KeyState<NW> ks;
@@ -265,6 +264,58 @@ __global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(Wa
   char* wbase = smem_raw + size_t(wib) * P.warp_smem;
   uint64_t* gkeys = P.gkeys ? P.gkeys + size_t(gwarp) * P.cap : nullptr;
   for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval, KS>(P, lay, wbase, gkeys, w, lane);
+}
+
+// Evaluator probe (sk_eval_states): the walk's own evaluator on caller-given
+// states.  Warp w loads half sequence w (+-1 int8), builds the state exactly
+// as the walk init does (skew expansion, O(L^2) sidelobes, Eval::init), writes
+// the raw delta vector (the trace row of _kernels.py:241-243), then applies
+// moves[w][0..M) one after another (apply_neighbor, _kernels.py:126-158, no
+// visited check), writing the delta vector after each.  Lets tests drive the
+// production evaluator on states a random walk never reaches (all +1,
+// periodic, published optima: |C_k| near its bound L - k).
+template <int NW, class Eval, int WPB>
+__global__ void __launch_bounds__(WPB * 32, 1) eval_states_kernel(WalkParams P, SmemLayout lay, const int8_t* halves,
+                                                                    int M, const int32_t* moves, int64_t* deltas) {
+  extern __shared__ __align__(128) char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int L = P.L, D = P.D, K = P.K;
+  char* wbase = smem_raw + size_t(wib) * P.warp_smem;
+  WarpSmem sm;
+  sm.s8 = reinterpret_cast<int8_t*>(wbase + lay.off_s8);
+  sm.ce = reinterpret_cast<int32_t*>(wbase + lay.off_ce);
+  sm.dl = reinterpret_cast<int32_t*>(wbase + lay.off_dl);
+  sm.occ = reinterpret_cast<uint32_t*>(wbase + lay.off_occ);
+  sm.keys = reinterpret_cast<uint64_t*>(wbase + lay.off_keys);
+  sm.ext = wbase + lay.off_ext;
+  int8_t* s = sm.s8 + lay.span_off;
+  for (int64_t w = int64_t(blockIdx.x) * WPB + wib; w < P.W; w += int64_t(gridDim.x) * WPB) {
+    for (int i = lane; i < int(lay.span); i += 32) sm.s8[i] = 0;
+    __syncwarp();
+    for (int h = lane; h < D; h += 32) s[h] = halves[w * D + h];
+    __syncwarp();
+    for (int i = 1 + lane; i < D; i += 32) s[D - 1 + i] = (i & 1) ? int8_t(-s[D - 1 - i]) : s[D - 1 - i];
+    __syncwarp();
+    for (int j = lane; j <= K; j += 32) {
+      int32_t acc = 0;
+      for (int i = 0; i < L - 2 * j; i++) acc += int32_t(s[i]) * int32_t(s[i + 2 * j]);
+      sm.ce[j] = acc;
+    }
+    __syncwarp();
+    Eval ev;
+    ev.init(P, sm, s, lane);
+    int64_t* row = deltas + w * int64_t(M + 1) * D;
+    ev.evaluate(P, sm, s, lane, row);
+    for (int m = 0; m < M; m++) {
+      __syncwarp();
+      const int h = moves[w * M + m];
+      if (h >= 0 && h < D) ev.apply(P, sm, s, h, lane);  // out of range: state unchanged
+      row += D;
+      ev.evaluate(P, sm, s, lane, row);
+    }
+    __syncwarp();
+  }
 }
 
 // Summary init / finish (tiny kernels on the same stream), one block per

@@ -11,8 +11,8 @@ Sharding: walkers [0, W) are split into contiguous slices, one per device
 (in-process ``devices=[...]``) or per rank (``process_group``, one process per
 GPU over NCCL).  Because seeds use the global walker index and the merge key
 carries it, a batch's result is identical for any device count.  Across
-ranks the exchange is one all-reduce MIN of the key and one all-reduce SUM of
-[steps, winner words (owner contributes, others add 0)] -- a few dozen bytes.
+ranks the exchange is one all_gather of every rank's summary [key, steps,
+words] (a few dozen bytes per rank), merged on the host.
 
 PyTorch is used only for device buffers, streams and torch.distributed.
 """
@@ -57,49 +57,41 @@ def decode_summary(raw: np.ndarray, nw: int) -> BatchResult | None:
 
 
 def merge_across_ranks(win: BatchResult | None, steps: int, nw: int, process_group, device) -> BatchResult:
-    """Merge per-rank batch results: the runner.py:252-256 rule (lowest E,
-    ties to the lowest global walker) is a MIN over (E << 32 | walker); steps
-    add up; the owner of the winning key contributes its words to a SUM in
-    which every other rank adds zeros.  Two tiny all-reduces per batch."""
-    import torch
-    import torch.distributed as dist
-
-    key = (win.best_E << 32) | win.walker if win is not None else (1 << 63) - 1
-    kt = torch.tensor([key], dtype=torch.int64, device=device)
-    dist.all_reduce(kt, op=dist.ReduceOp.MIN, group=process_group)
-    gkey = int(kt.item())
-    payload = np.zeros(1 + nw, dtype=np.int64)
-    payload[0] = steps
-    if win is not None and ((win.best_E << 32) | win.walker) == gkey:
-        payload[1:] = np.asarray(win.best_words, dtype=np.uint64).view(np.int64)
-    pt = torch.from_numpy(payload).to(device)
-    dist.all_reduce(pt, op=dist.ReduceOp.SUM, group=process_group)
-    pv = pt.cpu().numpy()
-    return BatchResult(gkey >> 32, gkey & 0xFFFFFFFF, int(pv[0]), pv[1:].view(np.uint64).copy())
+    """Merge per-rank batch results (one search); see merge_many_across_ranks."""
+    return merge_many_across_ranks([win], [steps], nw, process_group, device)[0]
 
 
 def merge_many_across_ranks(wins, steps, nw: int, process_group, device):
-    """merge_across_ranks for R searches at once: one all-reduce MIN over R
-    keys and one all-reduce SUM over R x (1 + nw) payload words."""
+    """Merge per-rank results of R searches with ONE collective: every rank
+    contributes its R summaries [key, steps, words...] (key = E << 32 |
+    global walker, runner.py:252-256's rule as a MIN; an empty slice sends
+    INT64_MAX) to an all_gather of R x (2 + nw) int64 words, then each rank
+    merges on the host: lowest key wins, steps add up (runner.py:250-256)."""
     import torch
     import torch.distributed as dist
 
     R = len(wins)
     big = (1 << 63) - 1
-    keys = np.array([((w.best_E << 32) | w.walker) if w is not None else big for w in wins], dtype=np.int64)
-    kt = torch.from_numpy(keys.copy()).to(device)
-    dist.all_reduce(kt, op=dist.ReduceOp.MIN, group=process_group)
-    gkeys = kt.cpu().numpy()
-    payload = np.zeros((R, 1 + nw), dtype=np.int64)
-    payload[:, 0] = steps
-    for r, w in enumerate(wins):
-        if w is not None and int(keys[r]) == int(gkeys[r]):
-            payload[r, 1:] = np.asarray(w.best_words, dtype=np.uint64).view(np.int64)
-    pt = torch.from_numpy(payload).to(device)
-    dist.all_reduce(pt, op=dist.ReduceOp.SUM, group=process_group)
-    pv = pt.cpu().numpy()
-    return [BatchResult(int(g) >> 32, int(g) & 0xFFFFFFFF, int(pv[r, 0]), pv[r, 1:].view(np.uint64).copy())
-            for r, g in enumerate(gkeys)]
+    row = np.zeros((R, 2 + nw), dtype=np.int64)
+    for r, (w, s) in enumerate(zip(wins, steps)):
+        row[r, 0] = ((w.best_E << 32) | w.walker) if w is not None else big
+        row[r, 1] = s
+        if w is not None:
+            row[r, 2:] = np.asarray(w.best_words, dtype=np.uint64).view(np.int64)
+    world = dist.get_world_size(process_group)
+    mine = torch.from_numpy(row).to(device)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=process_group)
+    allr = np.stack([p.cpu().numpy() for p in parts])  # [world, R, 2 + nw]
+    out = []
+    for r in range(R):
+        src = int(np.argmin(allr[:, r, 0]))
+        key = int(allr[src, r, 0])
+        if key == big:
+            raise RuntimeError("no rank produced a walk for this batch")
+        out.append(BatchResult(key >> 32, key & 0xFFFFFFFF, int(allr[:, r, 1].sum()),
+                               allr[src, r, 2:].view(np.uint64).copy()))
+    return out
 
 
 class BatchEngine:
@@ -110,7 +102,7 @@ class BatchEngine:
 
         self.torch = torch
         self.L = int(L)
-        self.n = int(n)
+        self.n = _lib.check_steps(n)
         self.D = (self.L + 1) // 2
         self.nw = (self.D + 63) // 64
         self.W = int(walkers)

@@ -57,3 +57,18 @@ def oracle():
 
     o.build()
     return o
+
+
+@pytest.fixture(scope="session")
+def golden_config2_traces():
+    return load_json("config2_traces.json")
+
+
+@pytest.fixture(scope="session")
+def golden_config_records():
+    return load_json("config_records.json")
+
+
+@pytest.fixture(scope="session")
+def golden_optima_43_55():
+    return load_json("optima_43_55.json")

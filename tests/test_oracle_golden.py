@@ -130,3 +130,54 @@ def test_exhaustive_range_slices_compose(oracle):
         e, g = min(parts)
         assert e == e_all and g ^ (g >> 1) == bits
         assert oracle.exhaustive_range(L, 0, total) == (e, g)
+
+
+# ---- BASELINE configs 1 and 2 (fixtures: oracle/gen_golden_r2.py) ----------
+def test_config2_traces(oracle, golden_config2_traces):
+    # run_walk_traced for derive_walk_seed(1, 0, w), w < 64, at L=101
+    g = golden_config2_traces
+    L, n = g["L"], g["n"]
+    d = (L + 1) // 2
+    assert len(g["walks"]) == 64
+    for w in g["walks"]:
+        seed = oracle.derive_walk_seed(g["master"], g["batch"], w["w"])
+        assert seed == int(w["seed"])
+        be, st, dead, bw, tw, td = oracle.saw_walk(L, n, seed, record=True)
+        assert (be, st, dead) == (w["best_E"], w["steps"], w["dead"]), w["w"]
+        piv = pivots_from_words(tw[: st + 1], d).astype(np.int8)
+        deltas = td[: st + (1 if dead else 0)]
+        assert sha(piv) == w["sha_pivots_i8"], w["w"]
+        assert sha(deltas.astype(np.int64)) == w["sha_deltas_i64"], w["w"]
+
+
+def test_config_records(oracle, golden_config_records):
+    # config 2's RunRecord (L=101, 4096 walkers, 2 batches) and config 1's
+    # records for all 100 master seeds at L=27 (target 37)
+    recs = golden_config_records["records"]
+    assert sum(1 for r in recs if r["config"]["L"] == 27) == 100
+    for item in recs:
+        cfg = item["config"]
+        got = oracle.solve_record(cfg["L"], cfg["walkers"], 8, cfg["master_seed"], cfg.get("max_nses"),
+                                  cfg.get("target_E"))
+        assert got == item["record"], cfg
+        if cfg["L"] == 27:
+            assert got["best_E"] == 37 and got["stop_reason"] == "target_reached"
+
+
+def test_optima_43_55_small_rows(oracle, golden_optima_43_55):
+    # the reference's exhaustive optima L=43..55; the CPU suite scans the two
+    # smallest rows, the GPU suite checks all of them (device + threaded oracle)
+    rows = {r["L"]: r for r in golden_optima_43_55["optima"]}
+    assert sorted(rows) == list(range(43, 56, 2))
+    for L in (43, 45):
+        e, bits = oracle.exhaustive_scan(L)
+        assert e == rows[L]["E"]
+        d = (L + 1) // 2
+        code = sum(1 << (d - 1 - h) for h in range(d) if (bits >> h) & 1)  # codec bit order
+        assert "0x" + format(code, f"0{-(-d // 4)}X") == rows[L]["hex"]
+
+
+def test_threaded_scan_equals_full_scan(oracle):
+    # the threaded slice scan the GPU suite uses as the L=55/59 checker
+    for L in (21, 31, 33):
+        assert oracle.exhaustive_scan_threaded(L, threads=4, slices=13) == oracle.exhaustive_scan(L), L

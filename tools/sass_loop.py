@@ -57,3 +57,7 @@ ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", t).split()[0].split(".")[
 print("opcodes:", ", ".join(f"{k}={v}" for k, v in ops.most_common(18)))
 lines = collections.Counter(f"{s[0]}:{s[1]}" for _, _, s in loop if s)
 print("top lines:", ", ".join(f"{k}={v}" for k, v in lines.most_common(25)))
+if os.environ.get("SASS_DUMP"):
+    with open(os.environ["SASS_DUMP"], "w") as f:
+        for a, t, s in loop:
+            f.write(f"{a:05x}  {t:70s}  {s[0] + ':' + str(s[1]) if s else ''}\n")
