@@ -1,0 +1,417 @@
+// eval_tc.cuh -- production neighbourhood evaluator for L <= 511 (SK_VARIANT_FAST).
+//
+// Same exact arithmetic as the reference's neighbor_delta / apply_neighbor
+// (_kernels.py:85-158), restated for one warp per walk:
+//
+//   dE(h) = 16 (c0 + 2 R_h - 2 s_x s_q) - xm s_p (X_h - s_q C_{q-p}),
+//   X_h   = sum_i T_pi[i] G(i - h'),   T_pi[i] = s_{2i+pi},  G(d) = C_{2|d|},
+//   p = h, q = L-1-h, pi = h & 1, h' = h >> 1, x = 3h - 2K, xm = 8 (4 at the centre).
+//
+// The correlation X_h of all D neighbours is one block-Toeplitz product on the
+// tensor cores (mma.sync.m16n8k16, f16 x f16 -> f32, exact: every operand is
+// a small integer, |C| <= L - 2 < 2048 and every partial sum < 2^24), laid out
+// so that each MMA costs four instructions:
+//
+//   A (16 x 16, the SIGNAL): row g <-> (pi = 0, block a = 8 tau + g),
+//     row g + 8 <-> (pi = 1, same a); A_m[row][k] = T_pi[8a + 16m + k].
+//     The four A registers of lane (g, t) are one 16-byte "Q record"
+//     {T0[e], T0[e+1], T1[e], T1[e+1], T0[e+8], T0[e+9], T1[e+8], T1[e+9]},
+//     e = 8a + 16m + 2t: ONE LDS.128, no register moves.
+//   B (16 x 8, the TOEPLITZ source): B_m[k][c] = G(16m + k - c), i.e. the
+//     pairs (G(x), G(x+1)) and (G(x+8), G(x+9)), x = 16m + 2t - g: two LDS.32
+//     from one of two copies of G (even- / odd-aligned pairs); x < 0 reads the
+//     mirrored pair and swaps its halves (G(-d) = G(d)).
+//   D: lane (g, t) holds the four CONSECUTIVE neighbours h0 + {0, 2, 1, 3},
+//     h0 = 128 tau + 16 g + 4 t, so the epilogue's per-neighbour operands
+//     (C_{q-p}, s_x, s_h) come from a few vector loads.
+//
+// A move (apply_neighbor, _kernels.py:126-158): every lane owns four
+// consecutive lags per 128 (j0 = 128 r + 4 l): C_{2j} -= 4 s_p v_j(h*) with
+// v_j = s_{p-2j} + s_{p+2j} (the flipped positions p, q read as zero, which
+// removes the excluded lag q - p and the own lag j = 0), computed as two
+// HADD2 + two HFMA2 on half2 registers from parity-split f16 spin arrays
+// (two shifted copies, so every spin pair is one aligned LDS.32), then
+// stored to both G copies.  R_h (sum_j s_{h-2j} s_{h+2j}) changes in O(1)
+// per neighbour.  Then 10 scattered cells (int8 sequence, f16 spin copies,
+// Q records) take the flipped spins: two stores.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "walk_engine.cuh"
+
+// Blocks per SM (4 warps each) the one- / two-tile kernels are register-capped
+// for; overridable at build time for experiments.
+#ifndef SK_TC_MIN_BLOCKS1
+#define SK_TC_MIN_BLOCKS1 4
+#endif
+#ifndef SK_TC_MIN_BLOCKS2
+#define SK_TC_MIN_BLOCKS2 3
+#endif
+
+namespace sk {
+
+constexpr int kTcMaxL = 511;  // D <= 256: at most two 128-neighbour tiles
+
+// Byte offsets inside the evaluator's shared-memory area (host and device).
+struct TcGeom {
+  int D, K, NI, MT;
+  int NT, TOFF;       // f16 spin arrays: NT halves each, index i at TOFF + i (+1 in the odd-aligned copy)
+  uint32_t q_off;     // Q records: record r in [-32, 8 NI + 24) at q_off + 16 (r + 32)
+  uint32_t ge_off;    // G(y), y in [-8, 128 MT + 8): even-aligned copy at ge_off + 2 (y + 8)
+  uint32_t go_off;    //                               odd-aligned copy at go_off + 2 (y + 9)
+  uint32_t t_off;     // [TA_0 | TB_0 | TA_1 | TB_1]: TA_pi[i] at +2 (i + TOFF), TB_pi[i] at +2 (i + TOFF + 1)
+  uint32_t s2_off;    // int8 S2[h] = 2 s_h (s_h at the centre h = K), h < D; 0 beyond
+  uint32_t bytes;
+};
+
+__host__ __device__ inline TcGeom tc_geom(int L) {
+  TcGeom g;
+  g.D = (L + 1) / 2;
+  g.K = g.D - 1;
+  g.NI = (g.D + 15) / 16;
+  g.MT = (g.NI + 7) / 8;
+  uint32_t o = 0;
+  g.q_off = o;
+  o += 16u * uint32_t(8 * g.NI + 56);
+  g.ge_off = o;
+  o += 2u * uint32_t(128 * g.MT + 16);
+  o = (o + 15u) & ~15u;
+  g.go_off = o;
+  o += 2u * uint32_t(128 * g.MT + 20);
+  o = (o + 15u) & ~15u;
+  g.NT = 3 * g.K + 20;
+  g.NT += g.NT & 1;
+  g.TOFF = g.K + 8;
+  g.TOFF += g.TOFF & 1;
+  g.t_off = o;
+  o += 8u * uint32_t(g.NT);
+  g.s2_off = o;
+  o += 128u * uint32_t(g.MT) + 16u;
+  g.bytes = (o + 31u) & ~31u;
+  return g;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld32s(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int32_t lds8(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(uint16_t(v)) : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t a, int32_t v) {
+  asm volatile("st.shared.s8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void mma_tc(float (&c)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+// Makes a value opaque to the compiler: per-walk constants set up once in
+// init() stay in registers instead of being recomputed inside the step loop.
+__device__ __forceinline__ void pin(uint32_t& v) { asm volatile("" : "+r"(v)); }
+__device__ __forceinline__ void pin(int32_t& v) { asm volatile("" : "+r"(v)); }
+__device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
+__device__ __forceinline__ __half2 u2h(uint32_t v) { return *reinterpret_cast<__half2*>(&v); }
+
+// NI = ceil(D / 16), compile time: every loop bound and MMA count below is a
+// constant (one instantiation per 16 lengths).
+template <int NI>
+struct EvalTC {
+  static constexpr int MT = (NI + 7) / 8;  // 128-neighbour tiles
+  static constexpr int CQ = MT;            // lag quads per lane (K < 128 MT)
+  static constexpr int M_LO = -(NI >> 1);  // k-blocks of the product
+  static constexpr int M_HI = NI - 1;
+  __host__ __device__ static constexpr int amax(int tau) { return (8 * tau + 7 < NI - 1) ? 8 * tau + 7 : NI - 1; }
+  __host__ __device__ static constexpr int mlo(int tau) { return -((amax(tau) + 1) >> 1); }
+  __host__ __device__ static constexpr int mhi(int tau) { return NI - 4 * tau - 1; }
+  // D-fragment register f <-> neighbour h0 + hoff(f)
+  __host__ __device__ static constexpr int hoff(int f) { return f == 1 ? 2 : (f == 2 ? 1 : f); }
+
+  // per-lane state
+  uint32_t qbase;           // this lane's Q record for tau = 0, m = 0
+  uint32_t b_pos, b_neg;    // B pair addresses at x0 = 2t - g (own-parity copy) / at -x0-1 (other copy)
+  uint32_t b_m0;            // m = 0 pair: b_pos if x0 >= 0 else b_neg (then swapped)
+  uint32_t sel_m0;          // byte_perm selector for it
+  uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile (s8 or G addresses)
+  int32_t Rk[MT][4];
+  uint32_t inv[MT][4];
+  uint32_t key[MT][4];
+  int32_t h0[MT];
+  int32_t xq_e, xq_o;       // 512 qs for the even / odd neighbours of a lane (qs = (-1)^(D-1-h))
+  int32_t m2xq_e, m2xq_o;   // -2 xq
+  __half2 cq[CQ][2];        // C_{2j}, j = j0 .. j0+3, j0 = 128 r + 4 lane (lag-owned)
+  // move-role constants (lanes 0..9): address = fb + f4 (x>>2) + 2 ((x>>1)&1) + f1 (x&1)
+  uint32_t fb, f4, f1;
+  uint32_t t_base, ge_a, go_a, s8_a;  // shared addresses
+
+  static uint32_t ext_bytes(int L, int) { return tc_geom(L).bytes; }
+  static bool supports(int L) { return L >= 3 && L <= kTcMaxL; }
+  static constexpr bool kNeedsDl = false;
+  static constexpr bool kSmemKeysVariant = true;
+  static constexpr bool kCeAliasKeys = true;
+  static constexpr int kMinBlocks = MT == 1 ? SK_TC_MIN_BLOCKS1 : SK_TC_MIN_BLOCKS2;
+  // s8 reads: R update 2h - x in [-(L-1), 2K + 12], s_{3h-2K} in [-2K, K + 18],
+  // position 0 kept 4-byte aligned (the s_h quad is one LDS.32)
+  static int span_lo(int L, int) { return (L + 8 + 3) & ~3; }
+  static int span_hi(int L, int) { return L + 16; }
+
+  __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
+    const TcGeom G = tc_geom(P.L);
+    const int D = P.D, K = P.K;
+    char* ext = reinterpret_cast<char*>(sm.ext);
+    const uint32_t ext_a = uint32_t(__cvta_generic_to_shared(ext));
+    for (uint32_t i = lane; i < G.bytes / 16u; i += 32) reinterpret_cast<uint4*>(ext)[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    __half* ge = reinterpret_cast<__half*>(ext + G.ge_off) + 8;
+    __half* go = reinterpret_cast<__half*>(ext + G.go_off) + 9;
+    for (int j = 1 + lane; j <= K; j += 32) {
+      const __half v = __int2half_rn(sm.ce[j]);
+      ge[j] = v;
+      go[j] = v;
+    }
+    __half* ta = reinterpret_cast<__half*>(ext + G.t_off);
+    __half* q = reinterpret_cast<__half*>(ext + G.q_off) + 8 * 32;
+    int8_t* s2 = reinterpret_cast<int8_t*>(ext + G.s2_off);
+    for (int h = lane; h < D; h += 32) s2[h] = int8_t(h == K ? s[h] : 2 * s[h]);
+    for (int x = lane; x < P.L; x += 32) {
+      const __half v = __int2half_rn(s[x]);
+      const int pi = x & 1, i = x >> 1;
+      ta[2 * pi * G.NT + G.TOFF + i] = v;
+      ta[(2 * pi + 1) * G.NT + G.TOFF + 1 + i] = v;
+      const int qo = 2 * pi + (i & 1);
+      q[8 * (i >> 1) + qo] = v;
+      q[8 * ((i >> 1) - 4) + 4 + qo] = v;
+    }
+    t_base = ext_a + G.t_off;
+    ge_a = ext_a + G.ge_off + 16u;  // address of G(0) in the even copy
+    go_a = ext_a + G.go_off + 18u;  // ... in the odd copy
+    s8_a = uint32_t(__cvta_generic_to_shared(s));
+    const int g = lane >> 2, t = lane & 3;
+    qbase = ext_a + G.q_off + 16u * uint32_t(32 + 4 * g + t);
+    const int x0 = 2 * t - g;
+    const uint32_t own = (g & 1) ? go_a : ge_a, oth = (g & 1) ? ge_a : go_a;
+    b_pos = own + uint32_t(2 * x0);
+    b_neg = oth + uint32_t(2 * (-x0 - 1));
+    b_m0 = x0 >= 0 ? b_pos : b_neg;
+    sel_m0 = x0 >= 0 ? 0x3210u : 0x1032u;
+    const int sigma = ((D - 1) & 1) ? -1 : 1;
+    xq_e = 512 * sigma;
+    xq_o = -512 * sigma;
+    m2xq_e = -2 * xq_e;
+    m2xq_o = -2 * xq_o;
+    const uint32_t s2_a = ext_a + G.s2_off;
+    const uint32_t cxcopy = ((K + 1) & 1) ? go_a : ge_a;  // parity of y0 = K - h0 - 3
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++) {
+      h0[tau] = 128 * tau + 16 * g + 4 * t;
+      const int h0a = h0[tau] <= K ? h0[tau] : (K & ~3);  // padding lanes read in-range cells
+      cxb[tau] = cxcopy + uint32_t(2 * (K - h0a - 3));
+      sxb[tau] = s8_a + uint32_t(3 * h0a - 2 * K);
+      shb[tau] = s2_a + uint32_t(h0a);
+      r2b[tau] = s8_a + uint32_t(2 * h0a);
+#pragma unroll
+      for (int f = 0; f < 4; f++) {
+        const int h = h0[tau] + hoff(f);
+        const bool live = h < D, centre = h == K;
+        const int pi = h & 1;
+        int32_t r = 0;
+        if (live && !centre)
+          for (int j = 1; 2 * j <= h; j++) r += int32_t(s[h - 2 * j]) * int32_t(s[h + 2 * j]);
+        const int32_t c0 = 16 * (centre ? (h >> 1) : (K - 1 - pi));
+        // the centre's s_x term is the constant S2[K] m2xq s_K = -2 xq (s_x = s_K): cancelled here
+        Rk[tau][f] = 64 * c0 + 2048 * r + (1 << 29) + h + (centre ? 2 * (f < 2 ? xq_e : xq_o) : 0);
+        inv[tau][f] = live ? 0u : ~0u;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < CQ; r++) {
+      int32_t c[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int j = 128 * r + 4 * lane + u;
+        c[u] = (j >= 1 && j <= K) ? sm.ce[j] : 0;
+      }
+      cq[r][0] = __halves2half2(__int2half_rn(c[0]), __int2half_rn(c[1]));
+      cq[r][1] = __halves2half2(__int2half_rn(c[2]), __int2half_rn(c[3]));
+    }
+    // move roles: 0,1 int8 sequence; 2,3 / 4,5 even- / odd-aligned f16 spin
+    // copies; 6,7 / 8,9 the two Q records holding the spin (even lane: p, odd: q)
+    // and lane 10 the S2 cell of p
+    const int role = lane >> 1;
+    fb = role == 0 ? s8_a
+                   : role == 1 ? t_base + 2u * G.TOFF
+                   : role == 2 ? t_base + 2u * G.NT + 2u * G.TOFF + 2u
+                   : role == 3 ? ext_a + G.q_off + 512u
+                   : role == 4 ? ext_a + G.q_off + 512u - 56u
+                               : s2_a;
+    f4 = (role == 0 || role >= 5) ? 4u : role <= 2 ? 4u : 16u;
+    f1 = (role == 0 || role >= 5) ? 1u : role <= 2 ? 4u * G.NT : 4u;
+    pin(qbase), pin(b_pos), pin(b_neg), pin(b_m0), pin(sel_m0), pin(xq_e), pin(xq_o), pin(m2xq_e), pin(m2xq_o);
+    pin(fb), pin(f4), pin(f1), pin(t_base), pin(ge_a), pin(go_a), pin(s8_a);
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++) {
+      pin(cxb[tau]), pin(sxb[tau]), pin(shb[tau]), pin(r2b[tau]), pin(h0[tau]);
+#pragma unroll
+      for (int f = 0; f < 4; f++) pin(inv[tau][f]);
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void evaluate(const WalkParams& P, WarpSmem&, const int8_t*, int, int64_t* trace_row) {
+    float acc[MT][2][4];
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++)
+#pragma unroll
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int o = 0; o < 4; o++) acc[tau][u][o] = 0.f;
+    // Y = sum_m A_m B_m over k-blocks m (B shared by the tiles)
+#pragma unroll
+    for (int m = M_LO; m <= M_HI; m++) {
+      uint32_t b0, b1;
+      if (m < 0) {  // both pairs mirrored: (G(x), G(x+1)) = swap(G(-x-1), G(-x))
+        b0 = __byte_perm(ld32s(b_neg - 32 * m), 0, 0x1032);
+        b1 = __byte_perm(ld32s(b_neg - 32 * m - 16), 0, 0x1032);
+      } else if (m == 0) {
+        b0 = __byte_perm(ld32s(b_m0), 0, sel_m0);
+        b1 = ld32s(b_pos + 16);
+      } else {
+        b0 = ld32s(b_pos + 32 * m);
+        b1 = ld32s(b_pos + 32 * m + 16);
+      }
+#pragma unroll
+      for (int tau = 0; tau < MT; tau++)
+        if (m >= mlo(tau) && m <= mhi(tau)) {
+          const uint4 a = lds128(qbase + 512u * tau + 128 * m);
+          mma_tc(acc[tau][(m - M_LO) & 1], a, b0, b1);
+        }
+    }
+    // key(h) = 64 dE + 2^29 + h = Rk + 512 qs C_{q-p} - s_h (xm 64 X + 2048 qs s_x)   (see header)
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++) {
+      const uint32_t cp1 = ld32s(cxb[tau]);       // (C_{q-p} of h0+3, of h0+2)
+      const uint32_t cp2 = ld32s(cxb[tau] + 4);   // (h0+1, h0)
+      const uint32_t shq = ld32s(shb[tau]);       // S2[h0 .. h0+3]
+      const __half2 c12 = u2h(cp1), c34 = u2h(cp2);
+      const int32_t cx[4] = {__half2int_rz(__high2half(c34)), __half2int_rz(__high2half(c12)),
+                             __half2int_rz(__low2half(c34)), __half2int_rz(__low2half(c12))};
+#pragma unroll
+      for (int f = 0; f < 4; f++) {
+        const int ho = hoff(f);
+        const int32_t X = __float2int_rz(acc[tau][0][f] + acc[tau][1][f]);
+        const int32_t sx = lds8(sxb[tau] + 3 * ho);
+        const int32_t sh = int32_t(__byte_perm(shq, 0, 0x8880u | (ho * 0x1110u + ho)));  // sign-extended byte ho
+        // S2 = 2 s_h: sh (-256 X - 2 xq s_x) = s_h (-512 X - 2048 qs s_x); at the
+        // centre S2 = s_K gives -256 s_K X and the constant cancelled in Rk
+        const int32_t k = Rk[tau][f] + (f < 2 ? xq_e : xq_o) * cx[f] + sh * (-256 * X + (f < 2 ? m2xq_e : m2xq_o) * sx);
+        if (trace_row && !inv[tau][f]) trace_row[h0[tau] + ho] = (k - (1 << 29) - (h0[tau] + ho)) >> 6;
+        key[tau][f] = uint32_t(k) | inv[tau][f];
+      }
+    }
+  }
+
+  __device__ __forceinline__ uint32_t local_min() const {
+    uint32_t m = kNoCand;
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++)
+#pragma unroll
+      for (int f = 0; f < 4; f++) m = min(m, key[tau][f]);
+    return m;
+  }
+
+  __device__ __forceinline__ void exclude(int h, int) {
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++) {
+      const int d = h - h0[tau];
+#pragma unroll
+      for (int f = 0; f < 4; f++)
+        if (d == hoff(f)) key[tau][f] = kNoCand;
+    }
+  }
+
+  __device__ __forceinline__ void apply(const WalkParams& P, WarpSmem&, int8_t*, int hs, int lane) {
+    const int K = P.K;
+    const int p = hs, q = P.L - 1 - hs;
+    const bool centre = (p == q);
+    const int32_t sp = lds8(s8_a + p), sq = lds8(s8_a + q);
+    // this lane's scattered cell (lanes 0..9): position x of the move
+    const int x = (lane & 1) ? q : p;
+    const int32_t sxo = (lane & 1) ? sq : sp;
+    const uint32_t fa = fb + f4 * uint32_t(x >> 2) + 2u * uint32_t((x >> 1) & 1) + f1 * uint32_t(x & 1);
+    __syncwarp();
+    // the flipped spins read as 0 while C and R are updated
+    if (lane < 2) sts8(fa, 0);
+    else if (lane < 6) sts16(fa, 0);
+    __syncwarp();
+    // C_{2j} += scale * v_j, v_j = s_{p-2j} + s_{p+2j} (apply_neighbor, _kernels.py:126-158)
+    {
+      const int P1 = p >> 1, pi = p & 1, par = P1 & 1;
+      const __half2 scale = __half2half2(__int2half_rn(centre ? -2 * sp : -4 * sp));
+      const TcGeom G = tc_geom(P.L);
+      const uint32_t ua = t_base + 2u * uint32_t(G.NT * (2 * pi + par) + P1 + G.TOFF + par);
+      const uint32_t ub = t_base + 2u * uint32_t(G.NT * (2 * pi + 1 - par) + P1 - 3 + G.TOFF + 1 - par);
+#pragma unroll
+      for (int r = 0; r < CQ; r++) {
+        const int j0 = 128 * r + 4 * lane;
+        if (j0 <= K) {
+          const uint32_t aa = ua + 2u * uint32_t(j0), ab = ub - 2u * uint32_t(j0);
+          const __half2 A0 = u2h(ld32s(aa)), A1 = u2h(ld32s(aa + 4));
+          const __half2 B0 = u2h(ld32s(ab)), B1 = u2h(ld32s(ab + 4));
+          const __half2 v01 = __hadd2(A0, __lowhigh2highlow(B1));
+          const __half2 v23 = __hadd2(A1, __lowhigh2highlow(B0));
+          cq[r][0] = __hfma2(v01, scale, cq[r][0]);
+          cq[r][1] = __hfma2(v23, scale, cq[r][1]);
+          const uint32_t c0 = h2u(cq[r][0]), c1v = h2u(cq[r][1]);
+          sts64(ge_a + 2u * uint32_t(j0), c0, c1v);
+          sts16(go_a + 2u * uint32_t(j0), c0);
+          sts32(go_a + 2u * uint32_t(j0) + 2u, __byte_perm(c0, c1v, 0x5432));
+          sts16(go_a + 2u * uint32_t(j0) + 6u, c1v >> 16);
+        }
+      }
+    }
+    // R_h: the terms s_y s_{2h-y}, y in {p, q}, change sign (same-parity
+    // neighbours; the zeroed cells drop the own term and, for a centre move,
+    // the pair that flips together)
+    {
+      const int32_t wp = -4096 * sp, wq = centre ? 0 : -4096 * sq;
+      const int pi = p & 1;
+#pragma unroll
+      for (int tau = 0; tau < MT; tau++) {
+        const uint32_t bp = r2b[tau] + uint32_t(2 * pi - p), bq = r2b[tau] + uint32_t(2 * pi - q);
+        const int32_t vp0 = lds8(bp), vp1 = lds8(bp + 4), vq0 = lds8(bq), vq1 = lds8(bq + 4);
+        const int32_t d0 = wp * vp0 + wq * vq0, d1 = wp * vp1 + wq * vq1;
+        if (pi == 0) {
+          Rk[tau][0] += d0;
+          Rk[tau][1] += d1;
+        } else {
+          Rk[tau][2] += d0;
+          Rk[tau][3] += d1;
+        }
+      }
+    }
+    __syncwarp();
+    // the flipped spins: int8 sequence, f16 spin copies, Q records
+    if (lane < 2 || lane == 10) sts8(fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
+    else if (lane < 10) sts16(fa, sxo > 0 ? 0xBC00u : 0x3C00u);
+    __syncwarp();
+  }
+};
+
+}  // namespace sk

@@ -19,6 +19,7 @@
 #include "../../include/sokol.h"
 #include "eval_scalar.cuh"
 #include "eval_fast.cuh"
+#include "eval_tc.cuh"
 #include "exhaustive.cuh"
 #include "neighborhood.cuh"
 #include "walk_engine.cuh"
@@ -207,6 +208,38 @@ int dispatch_fast_small(int L, F&& f) {
   return f(NWc{}, (sk::EvalFast<1, 0>*)nullptr);
 }
 
+// L <= 511: the one- / two-tile evaluator with a compile-time k-block count
+// (NI = ceil(D / 16) fixes the word count too: nw = ceil(NI / 4)).
+template <int NI, class F>
+int dispatch_tc_at(F&& f) {
+  return f(std::integral_constant<int, (NI + 3) / 4>{}, (sk::EvalTC<NI>*)nullptr);
+}
+
+template <class F>
+int dispatch_tc(int L, F&& f) {
+  switch (((L + 1) / 2 + 15) / 16) {
+    case 1: return dispatch_tc_at<1>(f);
+    case 2: return dispatch_tc_at<2>(f);
+    case 3: return dispatch_tc_at<3>(f);
+    case 4: return dispatch_tc_at<4>(f);
+    case 5: return dispatch_tc_at<5>(f);
+    case 6: return dispatch_tc_at<6>(f);
+    case 7: return dispatch_tc_at<7>(f);
+    case 8: return dispatch_tc_at<8>(f);
+#ifndef SK_TC_ONE_TILE_ONLY
+    case 9: return dispatch_tc_at<9>(f);
+    case 10: return dispatch_tc_at<10>(f);
+    case 11: return dispatch_tc_at<11>(f);
+    case 12: return dispatch_tc_at<12>(f);
+    case 13: return dispatch_tc_at<13>(f);
+    case 14: return dispatch_tc_at<14>(f);
+    case 15: return dispatch_tc_at<15>(f);
+    case 16: return dispatch_tc_at<16>(f);
+#endif
+  }
+  return fail(SK_ERR_UNSUPPORTED, "no EvalTC instantiation for this length");
+}
+
 template <class F>
 int dispatch_eval(int L, int nw, bool scalar, F&& f) {
   if (scalar) {
@@ -222,6 +255,13 @@ int dispatch_eval(int L, int nw, bool scalar, F&& f) {
     }
     return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
   }
+#ifndef SK_OLD_FAST_EVALUATOR
+#ifdef SK_TC_ONE_TILE_ONLY
+  if (L <= 255) return dispatch_tc(L, f);
+#else
+  if (L <= sk::kTcMaxL) return dispatch_tc(L, f);
+#endif
+#endif
   switch (nw) {
     case 1: return dispatch_fast_small<1>(L, f);
     case 2: return dispatch_fast_small<2>(L, f);

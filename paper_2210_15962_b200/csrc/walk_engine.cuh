@@ -188,6 +188,9 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   for (int step = 0; step < n; step++) {
     // ---- neighbourhood (_kernels.py:239-243) ----------------------------
     ev.evaluate(P, sm, s, lane, TRACE ? P.trace_deltas + (int64_t(w) * n + step) * D : nullptr);
+    // undoing the last move returns to P_{t-1}, whose key is in the set:
+    // rejected without hashing (the same membership answer)
+    if (last >= 0) ev.exclude(last, lane);
     // ---- best unvisited neighbour (_kernels.py:244-261) -----------------
     int hs = -1;
     int32_t dsel = 0;
@@ -195,10 +198,6 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
       const uint32_t m = warp_min_u32(ev.local_min());
       if (m == kNoCand) break;
       const int hc = cand_h(m);
-      if (hc == last) {  // undoing the last move returns to P_{t-1}, whose key is in the set
-        ev.exclude(hc, lane);
-        continue;
-      }
       uint64_t chain[NW];
       const uint64_t nk = ks.u_of_flip(words, D, hc, chain);
       if (!vs.probe<KS>(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
