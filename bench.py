@@ -258,19 +258,7 @@ def run_native(args):
     value = nse / (dev_ms / 1e3)
 
     # ---- roofline of the walk kernel (one launch per step) ----------------
-    tau = nse * D  # lag-terms; D per NSE
-    achieved_tops = tau * 2 / (dev_ms / 1e3) / 1e12 / max(1, world)  # per GPU: INT ops (1 MAC = 2 ops)
-    peaks = load_peaks()
-    ncu = load_ncu(L, Wg)
-    roof = {"bound": "int32", "achieved": achieved_tops, "peak": peaks["int_tops"], "unit": "Tops/s",
-            "frac": achieved_tops / peaks["int_tops"] if peaks["int_tops"] else None,
-            "traffic": ncu.get("traffic_bytes_per_launch"),
-            "ncu": ncu,
-            "peak_source": peaks["int_src"],
-            "algorithmic_unit": "lag-term tau = one (neighbour, even lag) v(2v-C) MAC; D*(D-1) per walk step, "
-                                f"D={D} per NSE; 2 INT32 ops per tau",
-            "tau_per_s_per_gpu": tau / (dev_ms / 1e3) / max(1, world)}
-
+    roof = roofline(L, n, Wg, value / max(1, world), dev_ms, clocks)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -360,6 +348,70 @@ def host_seeds(master, batch, begin, W):
         return np.ascontiguousarray(mix(h ^ w) & M)
 
 
+def mma_per_step(L: int) -> int:
+    """mma.sync.m16n8k16 per walk step of the production evaluator
+    (eval_tc.cuh for L <= 511: sum over 128-neighbour tiles of the k-block
+    range [mlo(tau), mhi(tau)]; eval_fast.cuh above: the padded block count
+    per 8-column tile)."""
+    D = (L + 1) // 2
+    if L <= 511:
+        NI = (D + 15) // 16
+        MT = (NI + 7) // 8
+        tot = 0
+        for tau in range(MT):
+            amax = min(8 * tau + 7, NI - 1)
+            tot += (NI - 4 * tau - 1) - (-((amax + 1) >> 1)) + 1
+        return tot
+    NB = ((D - 1) >> 1) // 16 + 1
+    NI = (D + 15) // 16
+    NT = (2 * NB + 7) // 8
+    return NT * (((NI - 1 + NB - 1 + 1) + 1) & ~1)
+
+
+def roofline(L, n, W, nse_per_s_gpu, dev_ms, clocks):
+    """The walk step is bound by instruction ISSUE: the
+    roofline is warp-instructions issued per second against 4 issue slots per
+    SM per clock at the measured clock.  Instructions per walk step come from
+    the committed ncu capture of this launch (profiles/ncu_walk_kernel.json);
+    the tensor pipe (HMMA count per step x steps/s against the measured
+    mma.sync rate) and the lag-term INT32 equivalence are reported beside it."""
+    D = (L + 1) // 2
+    steps_per_s = nse_per_s_gpu / (D - 1)
+    peaks = load_peaks()
+    ncu = load_ncu(L, W)
+    mhz = clocks.get("sm_mhz") or 1965.0
+    issue_peak = 148 * 4 * mhz * 1e6 / 1e9  # Gwarp-inst/s
+    ips = ncu.get("inst_per_walk_step")
+    achieved = ips * steps_per_s / 1e9 if ips else None
+    mma = mma_per_step(L)
+    tau = nse_per_s_gpu * D
+    return {
+        "bound": "issue",
+        "achieved": achieved,
+        "peak": issue_peak,
+        "unit": "Gwarp-inst/s",
+        "frac": achieved / issue_peak if achieved else None,
+        "traffic": ncu.get("traffic_bytes_per_launch"),
+        "inst_per_walk_step": ips,
+        "peak_source": f"148 SM x 4 schedulers x 1 warp-inst/clk at the run's median SM clock ({mhz:.0f} MHz)",
+        "pipes": {
+            "tensor": {"mma_per_step": mma, "achieved_mma_per_s": mma * steps_per_s,
+                       "peak_mma_per_s": peaks["hmma_per_s"],
+                       "frac": mma * steps_per_s / peaks["hmma_per_s"] if peaks["hmma_per_s"] else None,
+                       "peak_source": peaks["hmma_src"]},
+            "ncu": ncu,
+        },
+        "int32_equivalent": {
+            "note": "equivalence metric, not a ceiling: lag-terms x 2 INT32 ops / measured IMAD peak; the "
+                    "contraction runs on the tensor pipe, so values above 1 are expected",
+            "achieved": tau * 2 / 1e12, "peak": peaks["int_tops"], "unit": "Tops/s",
+            "frac": tau * 2 / 1e12 / peaks["int_tops"] if peaks["int_tops"] else None,
+            "algorithmic_unit": "lag-term tau = one (neighbour, even lag) v(2v-C) MAC; D*(D-1) per walk step, "
+                                f"D={D} per NSE",
+            "tau_per_s_per_gpu": tau},
+    }
+
+
 def load_ncu(L, W):
     """DRAM traffic and pipe utilisation of the walk kernel from the committed
     ncu --set full capture of this bench's launch (profiles/ncu_walk_kernel.json)."""
@@ -368,9 +420,12 @@ def load_ncu(L, W):
         return {}
     with open(p) as f:
         d = json.load(f)
-    out = {k: d[k] for k in ("source", "tensor_pipe_pct", "alu_pipe_pct", "lsu_pipe_pct", "issue_busy_pct",
-                             "warps_per_sm", "registers", "smem_wavefronts_pct", "smem_ld_bank_conflict_share")
+    out = {k: d[k] for k in ("source", "kernel", "tensor_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "lsu_pipe_pct",
+                             "issue_busy_pct", "warps_per_sm", "registers", "smem_wavefronts_pct",
+                             "smem_ld_bank_conflict_share", "stall_top")
            if k in d}
+    if d.get("L") == L and d.get("inst_executed") and d.get("walk_steps"):
+        out["inst_per_walk_step"] = d["inst_executed"] / d["walk_steps"]
     if d.get("L") == L and d.get("walks") and d.get("dram_bytes") is not None:
         out["traffic_bytes_per_launch"] = d["dram_bytes"] * (W / d["walks"])
         out["traffic_note"] = f"dram read+write of one captured launch ({d['walks']} walks), scaled to {W} walks"
@@ -378,9 +433,10 @@ def load_ncu(L, W):
 
 
 def load_peaks():
-    """INT32 peak: profiles/microbench (measured on B200 by tools/microbench.cu)
-    if present, else the theoretical 64 IMAD lanes/clk/SM x 148 x 1.965 GHz."""
-    out = {"int_tops": 2 * 148 * 64 * 1.965e9 / 1e12, "int_src": "theoretical IMAD 64 lanes/clk/SM x 148 SM x 1965 MHz (x2 ops)"}
+    """INT32 and mma.sync peaks: profiles/microbench_peaks.json (measured on
+    B200 by tools/microbench.cu) if present, else the theoretical IMAD rate."""
+    out = {"int_tops": 2 * 148 * 64 * 1.965e9 / 1e12, "int_src": "theoretical IMAD 64 lanes/clk/SM x 148 SM x 1965 MHz (x2 ops)",
+           "hmma_per_s": None, "hmma_src": None}
     p = os.path.join(ROOT, "profiles", "microbench_peaks.json")
     if os.path.exists(p):
         with open(p) as f:
@@ -388,8 +444,9 @@ def load_peaks():
         if mb.get("imad_tops"):
             out["int_tops"] = mb["imad_tops"]
             out["int_src"] = f"measured IMAD (profiles/microbench_peaks.json, {mb.get('when', '')})"
-        if mb.get("traffic_bytes_per_launch") is not None:
-            out["traffic_bytes_per_launch"] = mb["traffic_bytes_per_launch"]
+        if mb.get("hmma_m16n8k16_f16f32_per_s"):
+            out["hmma_per_s"] = mb["hmma_m16n8k16_f16f32_per_s"]
+            out["hmma_src"] = f"measured mma.sync.m16n8k16 f16->f32 (profiles/microbench_peaks.json, {mb.get('when', '')})"
     return out
 
 

@@ -91,32 +91,49 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
   return g;
 }
 
+// Shared-memory accesses by address (the layout is computed, not typed).  The
+// "memory" clobbers order them against the C++ stores of init() and of the
+// walk engine: an asm without one may be scheduled across ordinary stores.
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t ld32s(uint32_t a) {
   uint32_t v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ int32_t lds8(uint32_t a) {
   int32_t v;
-  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(uint16_t(v)) : "memory");
+// Predicated stores (one ISETP + @P STS, no divergent branch).
+__device__ __forceinline__ void sts8_if(bool c, uint32_t a, int32_t v) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p st.shared.s8 [%0], %1; }" ::"r"(a), "r"(v), "r"(int(c))
+               : "memory");
 }
-__device__ __forceinline__ void sts8(uint32_t a, int32_t v) {
-  asm volatile("st.shared.s8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+__device__ __forceinline__ void sts16_if(bool c, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p st.shared.b16 [%0], %1; }" ::"r"(a), "h"(uint16_t(v)),
+               "r"(int(c))
+               : "memory");
 }
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+__device__ __forceinline__ void sts32_if(bool c, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p st.shared.b32 [%0], %1; }" ::"r"(a), "r"(v), "r"(int(c))
+               : "memory");
 }
-__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+__device__ __forceinline__ void sts64_if(bool c, uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %3, 0; @p st.shared.v2.b32 [%0], {%1, %2}; }" ::"r"(a), "r"(x), "r"(y),
+               "r"(int(c))
+               : "memory");
+}
+// v if a != b else ~0 (a SEL; a plain ternary on an unrolled constant b can
+// become a jump table)
+__device__ __forceinline__ uint32_t mask_if_eq(uint32_t v, int a, int b) {
+  uint32_t r;
+  asm("{ .reg .pred p; setp.eq.s32 p, %1, %2; selp.b32 %0, -1, %3, p; }" : "=r"(r) : "r"(a), "r"(b), "r"(v));
+  return r;
 }
 __device__ __forceinline__ void mma_tc(float (&c)[4], const uint4& a, uint32_t b0, uint32_t b1) {
   asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -127,6 +144,13 @@ __device__ __forceinline__ void mma_tc(float (&c)[4], const uint4& a, uint32_t b
 // init() stay in registers instead of being recomputed inside the step loop.
 __device__ __forceinline__ void pin(uint32_t& v) { asm volatile("" : "+r"(v)); }
 __device__ __forceinline__ void pin(int32_t& v) { asm volatile("" : "+r"(v)); }
+// Byte B of x, sign-extended (one PRMT: the selector's bit 3 replicates the
+// sign; __byte_perm masks that bit off, so this is inline PTX).
+__device__ __forceinline__ int32_t sext_byte(uint32_t x, int b) {
+  int32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(b | ((b | 8) << 4) | ((b | 8) << 8) | ((b | 8) << 12)));
+  return r;
+}
 __device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
 __device__ __forceinline__ __half2 u2h(uint32_t v) { return *reinterpret_cast<__half2*>(&v); }
 
@@ -317,7 +341,7 @@ struct EvalTC {
         const int ho = hoff(f);
         const int32_t X = __float2int_rz(acc[tau][0][f] + acc[tau][1][f]);
         const int32_t sx = lds8(sxb[tau] + 3 * ho);
-        const int32_t sh = int32_t(__byte_perm(shq, 0, 0x8880u | (ho * 0x1110u + ho)));  // sign-extended byte ho
+        const int32_t sh = sext_byte(shq, ho);
         // S2 = 2 s_h: sh (-256 X - 2 xq s_x) = s_h (-512 X - 2048 qs s_x); at the
         // centre S2 = s_K gives -256 s_K X and the constant cancelled in Rk
         const int32_t k = Rk[tau][f] + (f < 2 ? xq_e : xq_o) * cx[f] + sh * (-256 * X + (f < 2 ? m2xq_e : m2xq_o) * sx);
@@ -342,7 +366,7 @@ struct EvalTC {
       const int d = h - h0[tau];
 #pragma unroll
       for (int f = 0; f < 4; f++)
-        if (d == hoff(f)) key[tau][f] = kNoCand;
+        key[tau][f] = mask_if_eq(key[tau][f], d, hoff(f));
     }
   }
 
@@ -357,8 +381,8 @@ struct EvalTC {
     const uint32_t fa = fb + f4 * uint32_t(x >> 2) + 2u * uint32_t((x >> 1) & 1) + f1 * uint32_t(x & 1);
     __syncwarp();
     // the flipped spins read as 0 while C and R are updated
-    if (lane < 2) sts8(fa, 0);
-    else if (lane < 6) sts16(fa, 0);
+    sts8_if(lane < 2, fa, 0);
+    sts16_if(lane >= 2 && lane < 6, fa, 0);
     __syncwarp();
     // C_{2j} += scale * v_j, v_j = s_{p-2j} + s_{p+2j} (apply_neighbor, _kernels.py:126-158)
     {
@@ -369,9 +393,12 @@ struct EvalTC {
       const uint32_t ub = t_base + 2u * uint32_t(G.NT * (2 * pi + 1 - par) + P1 - 3 + G.TOFF + 1 - par);
 #pragma unroll
       for (int r = 0; r < CQ; r++) {
+        // lanes past K read a valid quad (clamped) and store nothing: no branch
         const int j0 = 128 * r + 4 * lane;
-        if (j0 <= K) {
-          const uint32_t aa = ua + 2u * uint32_t(j0), ab = ub - 2u * uint32_t(j0);
+        const bool act = j0 <= K;
+        const int jr = act ? j0 : 0;
+        {
+          const uint32_t aa = ua + 2u * uint32_t(jr), ab = ub - 2u * uint32_t(jr);
           const __half2 A0 = u2h(ld32s(aa)), A1 = u2h(ld32s(aa + 4));
           const __half2 B0 = u2h(ld32s(ab)), B1 = u2h(ld32s(ab + 4));
           const __half2 v01 = __hadd2(A0, __lowhigh2highlow(B1));
@@ -379,10 +406,10 @@ struct EvalTC {
           cq[r][0] = __hfma2(v01, scale, cq[r][0]);
           cq[r][1] = __hfma2(v23, scale, cq[r][1]);
           const uint32_t c0 = h2u(cq[r][0]), c1v = h2u(cq[r][1]);
-          sts64(ge_a + 2u * uint32_t(j0), c0, c1v);
-          sts16(go_a + 2u * uint32_t(j0), c0);
-          sts32(go_a + 2u * uint32_t(j0) + 2u, __byte_perm(c0, c1v, 0x5432));
-          sts16(go_a + 2u * uint32_t(j0) + 6u, c1v >> 16);
+          sts64_if(act, ge_a + 2u * uint32_t(jr), c0, c1v);
+          sts16_if(act, go_a + 2u * uint32_t(jr), c0);
+          sts32_if(act, go_a + 2u * uint32_t(jr) + 2u, __byte_perm(c0, c1v, 0x5432));
+          sts16_if(act, go_a + 2u * uint32_t(jr) + 6u, c1v >> 16);
         }
       }
     }
@@ -408,8 +435,8 @@ struct EvalTC {
     }
     __syncwarp();
     // the flipped spins: int8 sequence, f16 spin copies, Q records
-    if (lane < 2 || lane == 10) sts8(fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
-    else if (lane < 10) sts16(fa, sxo > 0 ? 0xBC00u : 0x3C00u);
+    sts8_if(lane < 2 || lane == 10, fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
+    sts16_if(lane >= 2 && lane < 10, fa, sxo > 0 ? 0xBC00u : 0x3C00u);
     __syncwarp();
   }
 };

@@ -113,6 +113,17 @@ struct Plan {
   int64_t resident = 0;  // walks resident at once (grid warps)
 };
 
+// Shared-memory carve-up per visited-set layout for the evaluator Eval (its
+// area size and spin-array margins); recomputed for the evaluator a launch
+// actually instantiates.
+template <class Eval>
+void plan_layouts(Plan& pl) {
+  const int L = pl.P.L, D = pl.P.D;
+  for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++)
+    pl.lay[v] = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, v, Eval::ext_bytes(L, D), Eval::kNeedsDl,
+                                     Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
+}
+
 template <class Eval>
 Plan make_plan(int L, int n) {
   Plan pl{};
@@ -124,9 +135,7 @@ Plan make_plan(int L, int n) {
   pl.P.K = D - 1;
   pl.P.cap = uint32_t(visited_capacity(n));
   pl.smem_keys_ok = pl.P.cap * 8u <= kSmemKeysMax;
-  for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++)
-    pl.lay[v] = sk::SmemLayout::make(L, D - 1, D, pl.P.cap, v, Eval::ext_bytes(L, D), Eval::kNeedsDl,
-                                     Eval::span_hi(L, D), Eval::kCeAliasKeys, Eval::span_lo(L, D));
+  plan_layouts<Eval>(pl);
   return pl;
 }
 
@@ -138,6 +147,7 @@ Plan make_plan(int L, int n) {
 // the others decide at run time (KS = 0).
 template <int NW, bool TRACE, class Eval>
 int launch_nw(Plan& pl, cudaStream_t st, int dev) {
+  plan_layouts<Eval>(pl);
   using KernT = void (*)(sk::WalkParams, sk::SmemLayout);
   KernT kern[4] = {nullptr, sk::saw_walk_kernel<NW, TRACE, Eval, kWPB, 0>, nullptr, nullptr};
   kern[2] = kern[3] = kern[1];

@@ -1,0 +1,36 @@
+"""CPU check of the production evaluator's layout algebra (eval_tc.cuh).
+
+tools/tc_emulate.py restates EvalTC on a byte array with the kernel's own
+offsets: Q records gathered into the MMA's A fragments, the mirrored /
+swapped G pairs of the B fragments, the key epilogue (S2 signs, C_{q-p},
+s_{3h-2K}), the lag-quad C update through the shifted f16 spin copies, the
+R update and the scattered flip stores.  Every delta vector must equal the
+oracle's all_neighbor_deltas along a chain of moves (including centre and
+end moves), at one- and two-tile lengths.  The device itself is checked by
+the -m gpu suite; this pins the algebra without a GPU.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import tc_emulate  # noqa: E402
+
+
+@pytest.mark.parametrize("L", [3, 5, 7, 27, 63, 101, 129, 201, 253, 255, 257, 301, 449, 511])
+def test_emulated_evaluator_matches_oracle(oracle, L):
+    d = (L + 1) // 2
+    rng = np.random.default_rng(L)
+    for half in (np.ones(d, np.int64), rng.choice([-1, 1], size=d)):
+        em = tc_emulate.Emu(L, half)
+        s, c, _ = oracle.init_state(L, half.astype(np.int64))
+        np.testing.assert_array_equal(em.evaluate(), oracle.all_neighbor_deltas(L, s, c))
+        for h in [d - 1, 0, d - 1] + list(rng.integers(0, d, size=3)):
+            em.apply(int(h))
+            oracle.apply_neighbor(L, s, c, int(h))
+            np.testing.assert_array_equal(em.evaluate(), oracle.all_neighbor_deltas(L, s, c), err_msg=f"L={L} h={h}")

@@ -1,7 +1,11 @@
 """Extract the walk kernel's roofline evidence from an ncu --set full report
 into profiles/ncu_walk_kernel.json (read by bench.py for roofline.traffic).
 
-    python tools/ncu_to_json.py gpurun_out/prof_bench.ncu-rep L WALKS > profiles/ncu_walk_kernel.json
+    python tools/ncu_to_json.py gpurun_out/prof_bench.ncu-rep L WALKS [N] > profiles/ncu_walk_kernel.json
+
+N = steps per walk (default 8 * D): walk_steps = WALKS * N, from which
+bench.py derives warp-instructions per walk step (dead ends are negligible at
+n = 8 D; the captured launch's own step count can be passed instead).
 """
 import csv
 import json
@@ -9,6 +13,7 @@ import subprocess
 import sys
 
 rep, L, W = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+N = int(sys.argv[4]) if len(sys.argv) > 4 else 8 * ((L + 1) // 2)
 raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                                      text=True).stdout.splitlines()))
 names, units, vals = raw[0], raw[1], raw[2]
@@ -30,7 +35,7 @@ def get(key):
 
 out = {
     "source": rep.split("/")[-1] + " (ncu --set full --clock-control none, one timed bench launch)",
-    "L": L, "walks": W,
+    "L": L, "walks": W, "walk_steps": W * N,
     "kernel": vals[names.index("Kernel Name")] if "Kernel Name" in names else None,
     "duration_ns": get("gpu__time_duration.sum"),
     "dram_bytes": (get("dram__bytes_read.sum") or 0) + (get("dram__bytes_write.sum") or 0),
