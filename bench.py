@@ -369,31 +369,45 @@ def mma_per_step(L: int) -> int:
 
 
 def roofline(L, n, W, nse_per_s_gpu, dev_ms, clocks):
-    """The walk step is bound by instruction ISSUE: the
-    roofline is warp-instructions issued per second against 4 issue slots per
-    SM per clock at the measured clock.  Instructions per walk step come from
-    the committed ncu capture of this launch (profiles/ncu_walk_kernel.json);
-    the tensor pipe (HMMA count per step x steps/s against the measured
-    mma.sync rate) and the lag-term INT32 equivalence are reported beside it."""
+    """The walk step is bound by on-chip throughput, not HBM:
+    shared-memory wavefronts (128 B each, one per SM per clock) and
+    instruction issue (4 warp-instructions per SM per clock).  Per walk step
+    counts of both come from the committed ncu capture of this launch
+    (profiles/ncu_walk_kernel.json) and are multiplied by the live steps/s;
+    "bound" names the higher fraction.  The tensor pipe (HMMA count per step
+    x steps/s against the measured mma.sync rate) and the lag-term INT32
+    equivalence are reported beside it."""
     D = (L + 1) // 2
     steps_per_s = nse_per_s_gpu / (D - 1)
     peaks = load_peaks()
     ncu = load_ncu(L, W)
     mhz = clocks.get("sm_mhz") or 1965.0
     issue_peak = 148 * 4 * mhz * 1e6 / 1e9  # Gwarp-inst/s
+    smem_peak = 148 * 128 * mhz * 1e6 / 1e9  # GB/s: one 128-byte shared-memory wavefront per SM per clock
     ips = ncu.get("inst_per_walk_step")
-    achieved = ips * steps_per_s / 1e9 if ips else None
+    wps = ncu.get("smem_wavefronts_per_walk_step")
+    issue = ips * steps_per_s / 1e9 if ips else None
+    smem = wps * 128 * steps_per_s / 1e9 if wps else None
     mma = mma_per_step(L)
     tau = nse_per_s_gpu * D
+    cand = {"smem": (smem, smem_peak, "GB/s", "shared-memory data pipe: 148 SM x 128 B/clk (1 wavefront/clk) at the "
+                     f"run's median SM clock ({mhz:.0f} MHz)"),
+            "issue": (issue, issue_peak, "Gwarp-inst/s", "instruction issue: 148 SM x 4 schedulers x 1 warp-inst/clk "
+                      f"at the run's median SM clock ({mhz:.0f} MHz)")}
+    bound = max(cand, key=lambda k: (cand[k][0] or 0) / cand[k][1])
+    achieved, peak, unit, src = cand[bound]
     return {
-        "bound": "issue",
+        "bound": bound,
         "achieved": achieved,
-        "peak": issue_peak,
-        "unit": "Gwarp-inst/s",
-        "frac": achieved / issue_peak if achieved else None,
+        "peak": peak,
+        "unit": unit,
+        "frac": achieved / peak if achieved else None,
         "traffic": ncu.get("traffic_bytes_per_launch"),
-        "inst_per_walk_step": ips,
-        "peak_source": f"148 SM x 4 schedulers x 1 warp-inst/clk at the run's median SM clock ({mhz:.0f} MHz)",
+        "peak_source": src,
+        "per_walk_step": {"warp_inst": ips, "smem_wavefronts": wps, "mma": mma},
+        "issue": {"achieved": issue, "peak": issue_peak, "unit": "Gwarp-inst/s",
+                  "frac": issue / issue_peak if issue else None},
+        "smem": {"achieved": smem, "peak": smem_peak, "unit": "GB/s", "frac": smem / smem_peak if smem else None},
         "pipes": {
             "tensor": {"mma_per_step": mma, "achieved_mma_per_s": mma * steps_per_s,
                        "peak_mma_per_s": peaks["hmma_per_s"],
@@ -426,6 +440,8 @@ def load_ncu(L, W):
            if k in d}
     if d.get("L") == L and d.get("inst_executed") and d.get("walk_steps"):
         out["inst_per_walk_step"] = d["inst_executed"] / d["walk_steps"]
+        if d.get("smem_wavefronts"):
+            out["smem_wavefronts_per_walk_step"] = d["smem_wavefronts"] / d["walk_steps"]
     if d.get("L") == L and d.get("walks") and d.get("dram_bytes") is not None:
         out["traffic_bytes_per_launch"] = d["dram_bytes"] * (W / d["walks"])
         out["traffic_note"] = f"dram read+write of one captured launch ({d['walks']} walks), scaled to {W} walks"

@@ -151,6 +151,8 @@ struct EvalFast {
   static int cpl_for(int D) { return 4 * ((((D + 63) / 64) + 1) / 2); }
   static int span_hi(int L, int D) { return L - 1 + max(D - 1, 64 * cpl_for(D)); }
   static int span_lo(int L, int D) { return max(L + 1, 64 * cpl_for(D)); }
+  static uint32_t block_bytes(int) { return 0; }  // no per-block table
+  __device__ static void block_init(const WalkParams&, char*, int, int) {}
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
     G = fast_geom(P.L);

@@ -39,6 +39,8 @@ struct EvalScalar {
   static constexpr int kMinBlocks = 1;
   static int span_hi(int L, int) { return 2 * L - 2; }  // q + k
   static int span_lo(int L, int) { return L - 1; }      // p - k
+  static uint32_t block_bytes(int) { return 0; }  // no per-block table
+  __device__ static void block_init(const WalkParams&, char*, int, int) {}
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 

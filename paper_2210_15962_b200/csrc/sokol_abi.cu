@@ -159,8 +159,9 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   int sms = 0, max_optin = 0, per[4] = {0, 0, 0, 0};
   SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SK_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  pl.P.block_smem = Eval::block_bytes(pl.P.L);
   for (int v = SK_VISITED_SMEM; v <= SK_VISITED_GLOBAL; v++) {
-    const size_t smem = size_t(pl.lay[v].total) * kWPB;
+    const size_t smem = pl.P.block_smem + size_t(pl.lay[v].total) * kWPB;
     if (smem > size_t(max_optin) || (v == SK_VISITED_SMEM && !pl.smem_keys_ok)) continue;
     SK_CUDA(cudaFuncSetAttribute(kern[v], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[v], kern[v], kWPB * 32, smem));
@@ -177,7 +178,7 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
   const sk::SmemLayout lay = pl.lay[mode];
   pl.P.warp_smem = lay.total;
   pl.P.visited_mode = mode;
-  const size_t smem = size_t(lay.total) * kWPB;
+  const size_t smem = pl.P.block_smem + size_t(lay.total) * kWPB;
   const int64_t want = (pl.P.W + kWPB - 1) / kWPB;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms));
   pl.resident = int64_t(per_sm) * sms * kWPB;
@@ -637,8 +638,9 @@ int sk_eval_states(int L, int64_t S, const int8_t* d_halves, int M, const int32_
     const sk::SmemLayout lay = pl.lay[SK_VISITED_GLOBAL];  // no visited set: the smallest layout
     pl.P.W = S;
     pl.P.warp_smem = lay.total;
+    pl.P.block_smem = Eval::block_bytes(L);
     auto kern = sk::eval_states_kernel<decltype(nwc)::value, Eval, kWPB>;
-    const size_t smem = size_t(lay.total) * kWPB;
+    const size_t smem = pl.P.block_smem + size_t(lay.total) * kWPB;
     SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per = 0;
     SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kWPB * 32, smem));

@@ -40,6 +40,7 @@ struct WalkParams {
   const uint64_t* batches;
   int64_t W_rep;
   uint32_t warp_smem;       // bytes of dynamic smem per warp
+  uint32_t block_smem;      // bytes of the per-block area before the warp areas (Eval::block_bytes)
 };
 
 // Per-warp shared-memory carve-up.  Offsets are computed identically on host
@@ -51,6 +52,7 @@ struct WarpSmem {
   uint32_t* occ;  // visited occupancy bitmap
   uint64_t* keys; // visited keys (smem or global)
   void* ext;      // evaluator-private area
+  char* blk;      // per-block area shared by the block's warps (read-only after Eval::block_init)
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -99,7 +101,7 @@ constexpr int32_t kExcluded = 0x7fffffff;
 
 // KS = 1: the visited keys are in shared memory (compile-time; see VisitedSet)
 template <int NW, bool TRACE, class Eval, int KS>
-__device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayout& lay, char* wbase,
+__device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayout& lay, char* blk, char* wbase,
                                              uint64_t* gkeys_warp, int64_t w, int lane) {
   const int L = P.L, D = P.D, K = P.K, n = P.n;
   const int OFF = lay.span_off;
@@ -110,6 +112,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   sm.occ = reinterpret_cast<uint32_t*>(wbase + lay.off_occ);
   sm.keys = gkeys_warp ? gkeys_warp : reinterpret_cast<uint64_t*>(wbase + lay.off_keys);
   sm.ext = wbase + lay.off_ext;
+  sm.blk = blk;
   int8_t* s = sm.s8 + OFF;  // s[i] valid for i in [-span_lo, span_hi], zero outside [0, L)
 
   // ---- first pivot (_kernels.py:201-209) --------------------------------
@@ -260,9 +263,12 @@ __global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(Wa
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = int64_t(blockIdx.x) * WPB + wib;
   const int64_t nwarps = int64_t(gridDim.x) * WPB;
-  char* wbase = smem_raw + size_t(wib) * P.warp_smem;
+  Eval::block_init(P, smem_raw, int(threadIdx.x), int(blockDim.x));
+  __syncthreads();
+  char* wbase = smem_raw + P.block_smem + size_t(wib) * P.warp_smem;
   uint64_t* gkeys = P.gkeys ? P.gkeys + size_t(gwarp) * P.cap : nullptr;
-  for (int64_t w = gwarp; w < P.W; w += nwarps) run_one_walk<NW, TRACE, Eval, KS>(P, lay, wbase, gkeys, w, lane);
+  for (int64_t w = gwarp; w < P.W; w += nwarps)
+    run_one_walk<NW, TRACE, Eval, KS>(P, lay, smem_raw, wbase, gkeys, w, lane);
 }
 
 // Evaluator probe (sk_eval_states): the walk's own evaluator on caller-given
@@ -280,8 +286,11 @@ __global__ void __launch_bounds__(WPB * 32, 1) eval_states_kernel(WalkParams P, 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int L = P.L, D = P.D, K = P.K;
-  char* wbase = smem_raw + size_t(wib) * P.warp_smem;
+  Eval::block_init(P, smem_raw, int(threadIdx.x), int(blockDim.x));
+  __syncthreads();
+  char* wbase = smem_raw + P.block_smem + size_t(wib) * P.warp_smem;
   WarpSmem sm;
+  sm.blk = smem_raw;
   sm.s8 = reinterpret_cast<int8_t*>(wbase + lay.off_s8);
   sm.ce = reinterpret_cast<int32_t*>(wbase + lay.off_ce);
   sm.dl = reinterpret_cast<int32_t*>(wbase + lay.off_dl);
