@@ -153,6 +153,7 @@ struct EvalFast {
   static int span_lo(int L, int D) { return max(L + 1, 64 * cpl_for(D)); }
   static uint32_t block_bytes(int) { return 0; }  // no per-block table
   __device__ static void block_init(const WalkParams&, char*, int, int) {}
+  __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}  // nothing to prefetch
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
     G = fast_geom(P.L);

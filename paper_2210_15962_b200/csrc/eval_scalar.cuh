@@ -41,6 +41,7 @@ struct EvalScalar {
   static int span_lo(int L, int) { return L - 1; }      // p - k
   static uint32_t block_bytes(int) { return 0; }  // no per-block table
   __device__ static void block_init(const WalkParams&, char*, int, int) {}
+  __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}  // nothing to prefetch
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 

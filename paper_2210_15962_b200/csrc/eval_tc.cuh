@@ -28,15 +28,12 @@
 // A move (apply_neighbor, _kernels.py:126-158): every lane owns four
 // consecutive lags per 128 (j0 = 128 r + 4 l): C_{2j} -= 4 s_p v_j(h*) with
 // v_j = s_{p-2j} + s_{p+2j} (the flipped positions p, q read as zero, which
-// removes the excluded lag q - p and the own lag j = 0).  The spins come from
-// parity-split int8 arrays E_pi[i] = 1 - s_{2i+pi} (1 = no spin) held in four
-// copies offset by one byte, so any four consecutive entries are ONE aligned
-// LDS.32: the byte sums n_j = e_{p+2j} + e_{p-2j} (no carries, n <= 4) give
-// v_j = 2 - n_j, widened to half2 by PRMT with 0x64 high bytes (1024 + n) and
-// applied with HADD2 + HFMA2, then stored to both G copies.  R_h
-// (sum_j s_{h-2j} s_{h+2j}) changes in O(1) per neighbour, read from the same
-// arrays.  Then 15 scattered cells (int8 sequence, spin copies, S2, Q
-// records) take the flipped spins: two stores.
+// removes the excluded lag q - p and the own lag j = 0), computed as two
+// HADD2 + two HFMA2 on half2 registers from parity-split f16 spin arrays
+// (two shifted copies, so every spin pair is one aligned LDS.32), then
+// stored to both G copies.  R_h (sum_j s_{h-2j} s_{h+2j}) changes in O(1)
+// per neighbour.  Then 10 scattered cells (int8 sequence, f16 spin copies,
+// Q records) take the flipped spins: two stores.
 #pragma once
 #include <cuda_fp16.h>
 
@@ -58,11 +55,11 @@ constexpr int kTcMaxL = 511;  // D <= 256: at most two 128-neighbour tiles
 // Byte offsets inside the evaluator's shared-memory area (host and device).
 struct TcGeom {
   int D, K, NI, MT;
-  int NE, EOFF;       // int8 spin arrays: NE bytes each, copy c holds index i at EOFF + c + i
+  int NT, TOFF;       // f16 spin arrays: NT halves each, index i at TOFF + i (+1 in the odd-aligned copy)
   uint32_t q_off;     // Q records: record r in [-32, 8 NI + 24) at q_off + 16 (r + 32)
   uint32_t ge_off;    // G(y), y in [-8, 128 MT + 8): even-aligned copy at ge_off + 2 (y + 8)
   uint32_t go_off;    //                               odd-aligned copy at go_off + 2 (y + 9)
-  uint32_t e_off;     // E_{pi,c}, pi = 0..1, c = 0..3, at e_off + (4 pi + c) NE
+  uint32_t t_off;     // [TA_0 | TB_0 | TA_1 | TB_1]: TA_pi[i] at +2 (i + TOFF), TB_pi[i] at +2 (i + TOFF + 1)
   uint32_t s2_off;    // int8 S2[h] = 2 s_h (s_h at the centre h = K), h < D; 0 beyond
   uint32_t bytes;
 };
@@ -82,10 +79,12 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
   g.go_off = o;
   o += 2u * uint32_t(128 * g.MT + 20);
   o = (o + 15u) & ~15u;
-  g.NE = (3 * g.K + 24 + 3) & ~3;  // window starts in [-K-3, 2K+3], +3 bytes, +3 copy offset
-  g.EOFF = (g.K + 8 + 3) & ~3;
-  g.e_off = o;
-  o += 8u * uint32_t(g.NE);
+  g.NT = 3 * g.K + 20;
+  g.NT += g.NT & 1;
+  g.TOFF = g.K + 8;
+  g.TOFF += g.TOFF & 1;
+  g.t_off = o;
+  o += 8u * uint32_t(g.NT);
   g.s2_off = o;
   o += 128u * uint32_t(g.MT) + 16u;
   g.bytes = (o + 31u) & ~31u;
@@ -103,11 +102,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 __device__ __forceinline__ uint32_t ld32s(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t lds16u(uint32_t a) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ int32_t lds8(uint32_t a) {
@@ -187,42 +181,17 @@ struct EvalTC {
   int32_t xq_e, xq_o;       // 512 qs for the even / odd neighbours of a lane (qs = (-1)^(D-1-h))
   int32_t m2xq_e, m2xq_o;   // -2 xq
   __half2 cq[CQ][2];        // C_{2j}, j = j0 .. j0+3, j0 = 128 r + 4 lane (lag-owned)
-  // move-role constants (lanes 0..14): cell address = fb + (offset of position x in this
-  // lane's array kind, read from the block table at tabx + 8 x)
-  uint32_t fb, tabx;
-  uint32_t tab_a;           // per-move table (block_init): 16 bytes per half index h
-  uint32_t e_base, ge_a, go_a, s8_a;  // shared addresses (e_base: index 0 of E_{0,0} without its copy offset)
+  // move-role constants (lanes 0..9): address = fb + f4 (x>>2) + 2 ((x>>1)&1) + f1 (x&1)
+  uint32_t fb, f4, f1;
+  uint32_t t_base, ge_a, go_a, s8_a;  // shared addresses
 
   static uint32_t ext_bytes(int L, int) { return tc_geom(L).bytes; }
-
-  // Per-block table (shared by the block's walks; depends only on L):
-  //   [16 h]      for a move at h: the offsets (from e_base) of the two C-update
-  //               windows and of the two R-update windows, copies included;
-  //   [16 D + 8x] for position x: its cell offset in the int8 sequence / S2
-  //               (x), in a spin-array copy (x >> 1 + 4 NE (x & 1)) and in a Q
-  //               record (16 (x >> 2) + 2 ((x >> 1) & 1) + 4 (x & 1)).
-  // Replaces ~30 instructions of uniform address arithmetic per move by one
-  // broadcast LDS.128 and one LDS.U16.
-  static uint32_t block_bytes(int L) { return (16u * uint32_t((L + 1) / 2) + 8u * uint32_t(L) + 127u) & ~127u; }
-  __device__ static void block_init(const WalkParams& P, char* blk, int tid, int nth) {
-    const TcGeom G = tc_geom(P.L);
-    uint4* th = reinterpret_cast<uint4*>(blk);
-    for (int h = tid; h < P.D; h += nth) {
-      const int p = h, q = P.L - 1 - h, P1 = p >> 1, pi = p & 1;
-      const int ca = (-P1) & 3, cb = (3 - P1) & 3;
-      const int ip = pi - ((p + pi) >> 1), iq = pi - ((q + pi) >> 1);
-      const int cp = (-ip) & 3, cq2 = (-iq) & 3;
-      th[h] = make_uint4(uint32_t((4 * pi + ca) * G.NE + ca + P1), uint32_t((4 * pi + cb) * G.NE + cb + P1 - 3),
-                         uint32_t((4 * pi + cp) * G.NE + cp + ip), uint32_t((4 * pi + cq2) * G.NE + cq2 + iq));
-    }
-    uint16_t* tx = reinterpret_cast<uint16_t*>(blk + 16 * P.D);
-    for (int x = tid; x < P.L; x += nth) {
-      tx[4 * x] = uint16_t(x);
-      tx[4 * x + 1] = uint16_t((x >> 1) + 4 * G.NE * (x & 1));
-      tx[4 * x + 2] = uint16_t(16 * (x >> 2) + 2 * ((x >> 1) & 1) + 4 * (x & 1));
-      tx[4 * x + 3] = 0;
-    }
-  }
+  // No per-block table and no prefetch: both were measured (a table of the
+  // per-move window offsets and flip-cell offsets, loaded before the probe):
+  // +2% at L=301, -1.4% at L=201, so the addresses are computed.
+  static uint32_t block_bytes(int) { return 0; }
+  __device__ static void block_init(const WalkParams&, char*, int, int) {}
+  __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}
   static bool supports(int L) { return L >= 3 && L <= kTcMaxL; }
   static constexpr bool kNeedsDl = false;
   static constexpr bool kSmemKeysVariant = true;
@@ -247,22 +216,20 @@ struct EvalTC {
       ge[j] = v;
       go[j] = v;
     }
-    int8_t* ea = reinterpret_cast<int8_t*>(ext + G.e_off);
-    for (int i = lane; i < 2 * G.NE; i += 32) reinterpret_cast<uint32_t*>(ea)[i] = 0x01010101u;  // no spin
-    __syncwarp();
+    __half* ta = reinterpret_cast<__half*>(ext + G.t_off);
     __half* q = reinterpret_cast<__half*>(ext + G.q_off) + 8 * 32;
     int8_t* s2 = reinterpret_cast<int8_t*>(ext + G.s2_off);
     for (int h = lane; h < D; h += 32) s2[h] = int8_t(h == K ? s[h] : 2 * s[h]);
     for (int x = lane; x < P.L; x += 32) {
       const __half v = __int2half_rn(s[x]);
       const int pi = x & 1, i = x >> 1;
-#pragma unroll
-      for (int c = 0; c < 4; c++) ea[(4 * pi + c) * G.NE + G.EOFF + c + i] = int8_t(1 - s[x]);
+      ta[2 * pi * G.NT + G.TOFF + i] = v;
+      ta[(2 * pi + 1) * G.NT + G.TOFF + 1 + i] = v;
       const int qo = 2 * pi + (i & 1);
       q[8 * (i >> 1) + qo] = v;
       q[8 * ((i >> 1) - 4) + 4 + qo] = v;
     }
-    e_base = ext_a + G.e_off + uint32_t(G.EOFF);
+    t_base = ext_a + G.t_off;
     ge_a = ext_a + G.ge_off + 16u;  // address of G(0) in the even copy
     go_a = ext_a + G.go_off + 18u;  // ... in the odd copy
     s8_a = uint32_t(__cvta_generic_to_shared(s));
@@ -288,7 +255,7 @@ struct EvalTC {
       cxb[tau] = cxcopy + uint32_t(2 * (K - h0a - 3));
       sxb[tau] = s8_a + uint32_t(3 * h0a - 2 * K);
       shb[tau] = s2_a + uint32_t(h0a);
-      r2b[tau] = e_base + uint32_t(h0a);  // R-update windows: E arrays at h0 + (uniform offset)
+      r2b[tau] = s8_a + uint32_t(2 * h0a);
 #pragma unroll
       for (int f = 0; f < 4; f++) {
         const int h = h0[tau] + hoff(f);
@@ -314,23 +281,20 @@ struct EvalTC {
       cq[r][0] = __halves2half2(__int2half_rn(c[0]), __int2half_rn(c[1]));
       cq[r][1] = __halves2half2(__int2half_rn(c[2]), __int2half_rn(c[3]));
     }
-    // move roles (even lane: p, odd lane: q): 0,1 int8 sequence; 2..9 the
-    // four copies of the spin array (c = (lane - 2) >> 1); 10 the S2 cell of
-    // p; 11..14 the two Q records holding the spin
-    tab_a = uint32_t(__cvta_generic_to_shared(sm.blk));
-    uint32_t kind = 0;  // field of the per-position table: 0 identity, 1 spin array, 2 Q record
-    fb = s8_a;
-    if (lane >= 2 && lane < 10) {
-      const int c = (lane - 2) >> 1;
-      fb = e_base + uint32_t(c * G.NE + c), kind = 1;
-    } else if (lane == 10) {
-      fb = s2_a;
-    } else if (lane >= 11) {
-      fb = ext_a + G.q_off + 512u - (lane >= 13 ? 56u : 0u), kind = 2;
-    }
-    tabx = tab_a + 16u * uint32_t(D) + 2u * kind;
+    // move roles: 0,1 int8 sequence; 2,3 / 4,5 even- / odd-aligned f16 spin
+    // copies; 6,7 / 8,9 the two Q records holding the spin (even lane: p, odd: q)
+    // and lane 10 the S2 cell of p
+    const int role = lane >> 1;
+    fb = role == 0 ? s8_a
+                   : role == 1 ? t_base + 2u * G.TOFF
+                   : role == 2 ? t_base + 2u * G.NT + 2u * G.TOFF + 2u
+                   : role == 3 ? ext_a + G.q_off + 512u
+                   : role == 4 ? ext_a + G.q_off + 512u - 56u
+                               : s2_a;
+    f4 = (role == 0 || role >= 5) ? 4u : role <= 2 ? 4u : 16u;
+    f1 = (role == 0 || role >= 5) ? 1u : role <= 2 ? 4u * G.NT : 4u;
     pin(qbase), pin(b_pos), pin(b_neg), pin(b_m0), pin(sel_m0), pin(xq_e), pin(xq_o), pin(m2xq_e), pin(m2xq_o);
-    pin(fb), pin(tabx), pin(tab_a), pin(e_base), pin(ge_a), pin(go_a), pin(s8_a);
+    pin(fb), pin(f4), pin(f1), pin(t_base), pin(ge_a), pin(go_a), pin(s8_a);
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
       pin(cxb[tau]), pin(sxb[tau]), pin(shb[tau]), pin(r2b[tau]), pin(h0[tau]);
@@ -417,54 +381,55 @@ struct EvalTC {
     const int p = hs, q = P.L - 1 - hs;
     const bool centre = (p == q);
     const int32_t sp = lds8(s8_a + p), sq = lds8(s8_a + q);
-    // this lane's scattered cell (lanes 0..14): position x of the move
+    // this lane's scattered cell (lanes 0..9): position x of the move
     const int x = (lane & 1) ? q : p;
     const int32_t sxo = (lane & 1) ? sq : sp;
-    const uint32_t fa = fb + lds16u(tabx + 8u * uint32_t(x));
-    const uint4 mv = lds128(tab_a + 16u * uint32_t(hs));  // this move's window offsets
+    const uint32_t fa = fb + f4 * uint32_t(x >> 2) + 2u * uint32_t((x >> 1) & 1) + f1 * uint32_t(x & 1);
     __syncwarp();
-    // the flipped spins read as absent while C and R are updated (s8 = 0, e = 1)
-    sts8_if(lane < 10, fa, lane < 2 ? 0 : 1);
+    // the flipped spins read as 0 while C and R are updated
+    sts8_if(lane < 2, fa, 0);
+    sts16_if(lane >= 2 && lane < 6, fa, 0);
     __syncwarp();
-    const int pi = p & 1;
     // C_{2j} += scale * v_j, v_j = s_{p-2j} + s_{p+2j} (apply_neighbor, _kernels.py:126-158)
     {
+      const int P1 = p >> 1, pi = p & 1, par = P1 & 1;
       const __half2 scale = __half2half2(__int2half_rn(centre ? -2 * sp : -4 * sp));
-      const __half2 c1026 = __half2half2(__ushort_as_half(0x6402u));  // 1026
-      const uint32_t ua = e_base + mv.x, ub = e_base + mv.y;  // windows in the copies where they are aligned
+      const TcGeom G = tc_geom(P.L);
+      const uint32_t ua = t_base + 2u * uint32_t(G.NT * (2 * pi + par) + P1 + G.TOFF + par);
+      const uint32_t ub = t_base + 2u * uint32_t(G.NT * (2 * pi + 1 - par) + P1 - 3 + G.TOFF + 1 - par);
 #pragma unroll
       for (int r = 0; r < CQ; r++) {
-        // lanes past K read a valid window (clamped) and store nothing: no branch
+        // lanes past K read a valid quad (clamped) and store nothing: no branch
         const int j0 = 128 * r + 4 * lane;
         const bool act = j0 <= K;
-        const uint32_t jr = act ? uint32_t(j0) : 0u;
-        const uint32_t ea = ld32s(ua + jr);                          // e_{p+2j}, j = j0 .. j0+3
-        const uint32_t eb = __byte_perm(ld32s(ub - jr), 0, 0x0123);  // e_{p-2j}, same order
-        const uint32_t n = ea + eb;                                  // bytes n_j <= 4: no carries
-        const __half2 v01 = __hsub2(c1026, u2h(__byte_perm(n, 0x64646464u, 0x5140)));  // 2 - n_j
-        const __half2 v23 = __hsub2(c1026, u2h(__byte_perm(n, 0x64646464u, 0x7362)));
-        cq[r][0] = __hfma2(v01, scale, cq[r][0]);
-        cq[r][1] = __hfma2(v23, scale, cq[r][1]);
-        const uint32_t c0 = h2u(cq[r][0]), c1v = h2u(cq[r][1]);
-        sts64_if(act, ge_a + 2u * jr, c0, c1v);
-        sts16_if(act, go_a + 2u * jr, c0);
-        sts32_if(act, go_a + 2u * jr + 2u, __byte_perm(c0, c1v, 0x5432));
-        sts16_if(act, go_a + 2u * jr + 6u, c1v >> 16);
+        const int jr = act ? j0 : 0;
+        {
+          const uint32_t aa = ua + 2u * uint32_t(jr), ab = ub - 2u * uint32_t(jr);
+          const __half2 A0 = u2h(ld32s(aa)), A1 = u2h(ld32s(aa + 4));
+          const __half2 B0 = u2h(ld32s(ab)), B1 = u2h(ld32s(ab + 4));
+          const __half2 v01 = __hadd2(A0, __lowhigh2highlow(B1));
+          const __half2 v23 = __hadd2(A1, __lowhigh2highlow(B0));
+          cq[r][0] = __hfma2(v01, scale, cq[r][0]);
+          cq[r][1] = __hfma2(v23, scale, cq[r][1]);
+          const uint32_t c0 = h2u(cq[r][0]), c1v = h2u(cq[r][1]);
+          sts64_if(act, ge_a + 2u * uint32_t(jr), c0, c1v);
+          sts16_if(act, go_a + 2u * uint32_t(jr), c0);
+          sts32_if(act, go_a + 2u * uint32_t(jr) + 2u, __byte_perm(c0, c1v, 0x5432));
+          sts16_if(act, go_a + 2u * uint32_t(jr) + 6u, c1v >> 16);
+        }
       }
     }
     // R_h: the terms s_y s_{2h-y}, y in {p, q}, change sign (same-parity
-    // neighbours h = h0 + pi + {0, 2}; the absent cells drop the own term and,
-    // for a centre move, the pair that flips together).  s_{2h-y} = 1 - e: the
-    // window of E_pi starting at h0 + pi - (y + pi) / 2, bytes 0 and 2.
+    // neighbours; the zeroed cells drop the own term and, for a centre move,
+    // the pair that flips together)
     {
       const int32_t wp = -4096 * sp, wq = centre ? 0 : -4096 * sq;
-      const uint32_t op = mv.z, oq = mv.w;
+      const int pi = p & 1;
 #pragma unroll
       for (int tau = 0; tau < MT; tau++) {
-        const uint32_t wpw = ld32s(r2b[tau] + op), wqw = ld32s(r2b[tau] + oq);
-        const int32_t wpq = wp + wq;
-        const int32_t d0 = wpq - wp * int32_t(__byte_perm(wpw, 0, 0x4440)) - wq * int32_t(__byte_perm(wqw, 0, 0x4440));
-        const int32_t d1 = wpq - wp * int32_t(__byte_perm(wpw, 0, 0x4442)) - wq * int32_t(__byte_perm(wqw, 0, 0x4442));
+        const uint32_t bp = r2b[tau] + uint32_t(2 * pi - p), bq = r2b[tau] + uint32_t(2 * pi - q);
+        const int32_t vp0 = lds8(bp), vp1 = lds8(bp + 4), vq0 = lds8(bq), vq1 = lds8(bq + 4);
+        const int32_t d0 = wp * vp0 + wq * vq0, d1 = wp * vp1 + wq * vq1;
         if (pi == 0) {
           Rk[tau][0] += d0;
           Rk[tau][1] += d1;
@@ -475,9 +440,9 @@ struct EvalTC {
       }
     }
     __syncwarp();
-    // the flipped spins: int8 sequence, spin-array copies (e = 1 - s), S2, Q records
-    sts8_if(lane <= 10, fa, lane < 2 ? -sxo : (lane < 10 ? 1 + sxo : (centre ? -sp : -2 * sp)));
-    sts16_if(lane >= 11 && lane < 15, fa, sxo > 0 ? 0xBC00u : 0x3C00u);
+    // the flipped spins: int8 sequence, f16 spin copies, Q records
+    sts8_if(lane < 2 || lane == 10, fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
+    sts16_if(lane >= 2 && lane < 10, fa, sxo > 0 ? 0xBC00u : 0x3C00u);
     __syncwarp();
   }
 };

@@ -201,6 +201,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
       const uint32_t m = warp_min_u32(ev.local_min());
       if (m == kNoCand) break;
       const int hc = cand_h(m);
+      ev.prefetch(P, hc, lane);  // the move's operands load while the candidate is probed
       uint64_t chain[NW];
       const uint64_t nk = ks.u_of_flip(words, D, hc, chain);
       if (!vs.probe<KS>(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)

@@ -1,7 +1,7 @@
 """Host emulation of EvalTC's shared-memory layout and fragment algebra.
 
 Mirrors paper_2210_15962_b200/csrc/eval_tc.cuh byte for byte: the Q records,
-the two G copies, the parity-split int8 spin arrays (four alignment copies), S2 and the int8 sequence
+the two G copies, the parity-split f16 spin copies, S2 and the int8 sequence
 live in one bytearray per walk; every lane's MMA fragments are gathered from
 it with the kernel's own address arithmetic and multiplied out, the keys are
 formed exactly as the epilogue does, and moves go through the same scattered
@@ -32,10 +32,12 @@ class Geom:
         self.go_off = o
         o += 2 * (128 * self.MT + 20)
         o = (o + 15) & ~15
-        self.NE = (3 * self.K + 24 + 3) & ~3
-        self.EOFF = (self.K + 8 + 3) & ~3
-        self.e_off = o
-        o += 8 * self.NE
+        self.NT = 3 * self.K + 20
+        self.NT += self.NT & 1
+        self.TOFF = self.K + 8
+        self.TOFF += self.TOFF & 1
+        self.t_off = o
+        o += 8 * self.NT
         self.s2_off = o
         o += 128 * self.MT + 16
         self.bytes = (o + 31) & ~31
@@ -78,13 +80,11 @@ class Emu:
             self.st16(g.go_off + 18 + 2 * j, H(C[j]))
         for h in range(D):
             self.ext[g.s2_off + h] = (int(s[h]) if h == K else 2 * int(s[h])) & 0xFF
-        for b in range(8 * g.NE):
-            self.ext[g.e_off + b] = 1  # e = 1 - s: 1 = no spin (zero padding)
         for x in range(L):
             v = H(s[x])
             pi, i = x & 1, x >> 1
-            for c in range(4):
-                self.ext[self.eaddr(pi, c, i)] = 1 - int(s[x])
+            self.st16(g.t_off + 2 * (2 * pi * g.NT + g.TOFF + i), v)
+            self.st16(g.t_off + 2 * ((2 * pi + 1) * g.NT + g.TOFF + 1 + i), v)
             qo = 2 * pi + (i & 1)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * (i >> 1) + qo), v)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * ((i >> 1) - 4) + 4 + qo), v)
@@ -114,18 +114,6 @@ class Emu:
                 for u in range(4):
                     j = 128 * r + 4 * lane + u
                     self.cq[lane, r, u] = H(C[j] if 1 <= j <= K else 0)
-
-    def eaddr(self, pi, c, i):
-        """E_{pi,c}[i]: copy c holds index i at offset EOFF + c + i, so a window
-        starting at i is 4-byte aligned in copy (-i) & 3."""
-        g = self.g
-        return g.e_off + (4 * pi + c) * g.NE + g.EOFF + c + i
-
-    def ewin(self, pi, i0):
-        c = (-i0) & 3
-        a = self.eaddr(pi, c, i0)
-        assert a % 4 == 0
-        return [self.ext[a + u] for u in range(4)]
 
     # byte-level access ------------------------------------------------------
     def st16(self, off, v):
@@ -219,24 +207,30 @@ class Emu:
         p, q = hs, L - 1 - hs
         centre = p == q
         sp, sq = self.s8v(p), self.s8v(q)
-        # zero pass: s8 = 0, e = 1 (no spin) in every copy
+        # zero pass
         for x in {p, q}:
             self.s8[g.span_lo + x] = 0
-            for c in range(4):
-                self.ext[self.eaddr(x & 1, c, x >> 1)] = 1
-        P1, pi = p >> 1, p & 1
+            pi, i = x & 1, x >> 1
+            self.st16(g.t_off + 2 * (2 * pi * g.NT + g.TOFF + i), H(0))
+            self.st16(g.t_off + 2 * ((2 * pi + 1) * g.NT + g.TOFF + 1 + i), H(0))
+        P1, pi, par = p >> 1, p & 1, (p >> 1) & 1
         scale = H(-2 * sp if centre else -4 * sp)
+        ua = g.t_off + 2 * (g.NT * (2 * pi + par) + P1 + g.TOFF + par)
+        ub = g.t_off + 2 * (g.NT * (2 * pi + 1 - par) + P1 - 3 + g.TOFF + 1 - par)
         for lane in range(32):
             for r in range(g.MT):
                 j0 = 128 * r + 4 * lane
                 if j0 > K:
                     continue
-                a = self.ewin(pi, P1 + j0)          # e at j0 .. j0+3 (p + 2j side)
-                b = self.ewin(pi, P1 - j0 - 3)      # e at j0+3 .. j0 (p - 2j side)
-                n = [a[u] + b[3 - u] for u in range(4)]
+                aa, ab = ua + 2 * j0, ub - 2 * j0
+                assert aa % 4 == 0 and ab % 4 == 0
+                A0 = (self.ld16(aa), self.ld16(aa + 2))
+                A1 = (self.ld16(aa + 4), self.ld16(aa + 6))
+                B0 = (self.ld16(ab), self.ld16(ab + 2))
+                B1 = (self.ld16(ab + 4), self.ld16(ab + 6))
+                v = [A0[0] + B1[1], A0[1] + B1[0], A1[0] + B0[1], A1[1] + B0[0]]
                 for u in range(4):
-                    v = H(1026.0 - float(H(1024 + n[u])))   # 2 - n = s_{p+2j} + s_{p-2j}
-                    self.cq[lane, r, u] = H(float(v) * float(scale) + float(self.cq[lane, r, u]))
+                    self.cq[lane, r, u] = H(float(v[u]) * float(scale) + float(self.cq[lane, r, u]))
                 for u in range(4):
                     self.st16(g.ge_off + 16 + 2 * (j0 + u), self.cq[lane, r, u])
                     self.st16(g.go_off + 18 + 2 * (j0 + u), self.cq[lane, r, u])
@@ -246,11 +240,9 @@ class Emu:
             for tau in range(g.MT):
                 h0 = 128 * tau + 16 * gg + 4 * t
                 h0a = h0 if h0 <= K else (K & ~3)
-                # s_{2h-x} for h = h0a + pi + {0, 2}: E_pi window at h0a + pi - (x + pi) / 2, bytes 0 and 2
-                wpn = self.ewin(pi, h0a + pi - (p + pi) // 2)
-                wqn = self.ewin(pi, h0a + pi - (q + pi) // 2)
-                vp0, vp1 = 1 - wpn[0], 1 - wpn[2]
-                vq0, vq1 = 1 - wqn[0], 1 - wqn[2]
+                base = 2 * h0a + 2 * pi
+                vp0, vp1 = self.s8v(base - p), self.s8v(base + 4 - p)
+                vq0, vq1 = self.s8v(base - q), self.s8v(base + 4 - q)
                 f0 = 0 if pi == 0 else 2
                 self.Rk[lane, tau, f0] += wp * vp0 + wq * vq0
                 self.Rk[lane, tau, f0 + 1] += wp * vp1 + wq * vq1
@@ -259,8 +251,8 @@ class Emu:
             self.s8[g.span_lo + x] = (-sxo) & 0xFF
             v = H(-sxo)
             pi2, i = x & 1, x >> 1
-            for c in range(4):
-                self.ext[self.eaddr(pi2, c, i)] = 1 + sxo
+            self.st16(g.t_off + 2 * (2 * pi2 * g.NT + g.TOFF + i), v)
+            self.st16(g.t_off + 2 * ((2 * pi2 + 1) * g.NT + g.TOFF + 1 + i), v)
             qo = 2 * pi2 + (i & 1)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * (i >> 1) + qo), v)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * ((i >> 1) - 4) + 4 + qo), v)
