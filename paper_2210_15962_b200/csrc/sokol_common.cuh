@@ -71,10 +71,12 @@ struct KeyState {
 
   // u of the pivot with half index h flipped; chain[] receives the candidate's
   // prefixes (valid from its flipped word on) for commit().
-  __device__ __forceinline__ uint64_t u_of_flip(const uint64_t (&w)[NW], int D, int h, uint64_t (&chain)[NW]) const {
+  // wi / bit receive the flipped word and bit (for toggle_word on acceptance).
+  __device__ __forceinline__ uint64_t u_of_flip(const uint64_t (&w)[NW], int D, int h, uint64_t (&chain)[NW],
+                                                int& wi, uint64_t& bit) const {
     const int b = D - 1 - h;
-    const int wi = b >> 6;
-    const uint64_t bit = 1ull << (b & 63);
+    wi = b >> 6;
+    bit = 1ull << (b & 63);
     if constexpr (NW == 1) {
       return hp[0] ^ w[0] ^ bit;
     } else if constexpr (NW == 2) {
@@ -104,6 +106,19 @@ struct KeyState {
     }
   }
 };
+
+// words ^= bit in word wi (wi, bit from KeyState::u_of_flip); wi is warp-uniform
+template <int NW>
+__device__ __forceinline__ void toggle_word(uint64_t (&w)[NW], int wi, uint64_t bit) {
+  if constexpr (NW == 1) {
+    w[0] ^= bit;
+  } else if constexpr (NW == 2) {
+    if (wi) w[1] ^= bit; else w[0] ^= bit;  // warp-uniform: predicated XORs
+  } else {
+#pragma unroll
+    for (int i = 0; i < NW; i++) w[i] ^= (wi == i) ? bit : 0ull;
+  }
+}
 
 template <int NW>
 __device__ __forceinline__ void toggle_half_bit(uint64_t (&w)[NW], int D, int h) {

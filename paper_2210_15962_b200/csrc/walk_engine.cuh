@@ -197,13 +197,15 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
     // ---- best unvisited neighbour (_kernels.py:244-261) -----------------
     int hs = -1;
     int32_t dsel = 0;
+    int fwi = 0;
+    uint64_t fbit = 0;
     for (;;) {
       const uint32_t m = warp_min_u32(ev.local_min());
       if (m == kNoCand) break;
       const int hc = cand_h(m);
       ev.prefetch(P, hc, lane);  // the move's operands load while the candidate is probed
       uint64_t chain[NW];
-      const uint64_t nk = ks.u_of_flip(words, D, hc, chain);
+      const uint64_t nk = ks.u_of_flip(words, D, hc, chain, fwi, fbit);
       if (!vs.probe<KS>(nk, lane, true)) {  // absent: inserted = _visited_add(best_key)
         hs = hc;
         dsel = cand_delta(m);
@@ -220,7 +222,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
     ev.apply(P, sm, s, hs, lane);
     last = hs;
     E += dsel;
-    toggle_half_bit<NW>(words, D, hs);
+    toggle_word<NW>(words, fwi, fbit);  // the accepted candidate's flip (last u_of_flip)
     steps += 1;
     if (TRACE) {
       if (lane < nw_rt) {
@@ -230,7 +232,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
         P.trace_words[(int64_t(w) * (n + 1) + steps) * nw_rt + lane] = v;
       }
     }
-    if (E < best_e) {
+    if (__builtin_expect(E < best_e, 0)) {  // rare after the first descent: a uniform branch, not selects
       best_e = E;
 #pragma unroll
       for (int i = 0; i < NW; i++) best_w[i] = words[i];

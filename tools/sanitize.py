@@ -29,10 +29,12 @@ def main():
     W = int(os.environ.get("SANITIZE_W", "48"))
     lib = _lib.load()
     bad = 0
-    for L in (27, 101, 201, 449):
+    lengths = [int(x) for x in os.environ.get("SANITIZE_LENGTHS", "27,101,201,449").split(",")]
+    for L in lengths:
         d = (L + 1) // 2
         n = 8 * d
-        for layout in (_lib.VISITED_SMEM, _lib.VISITED_FINGERPRINT, _lib.VISITED_GLOBAL):
+        layouts = [int(x) for x in os.environ.get("SANITIZE_LAYOUTS", "1,2,3").split(",")]
+        for layout in layouts:
             for variant in (_lib.VARIANT_FAST, _lib.VARIANT_SCALAR):
                 _lib.set_variant(variant)
                 _lib.set_visited_layout(layout)
