@@ -21,6 +21,16 @@ from .core import (
 )
 from .neighborhood import EvalState, apply_flip, compute_deltas, flip, naive_oracle
 from .published import BEST_KNOWN, KnownResult
+from .stats import (
+    PUBLISHED_TREND,
+    ExpFit,
+    TrendModel,
+    anderson_darling_exponential,
+    fit_exponential,
+    fit_lambda_trend,
+    nses_limit,
+    optimality_probability,
+)
 from .runner import (
     RunConfig,
     RunRecord,
@@ -47,7 +57,8 @@ __version__ = "0.1.0"
 __all__ = [
     "DecodeError", "decode", "encode", "EnergyRecord", "autocorrelation", "autocorrelations", "energy",
     "expand_skew", "half_dim", "merit_factor", "sidelobe_array", "EvalState", "apply_flip", "compute_deltas",
-    "flip", "naive_oracle", "BEST_KNOWN", "KnownResult", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
+    "flip", "naive_oracle", "BEST_KNOWN", "KnownResult", "PUBLISHED_TREND", "ExpFit", "TrendModel",
+    "anderson_darling_exponential", "fit_exponential", "fit_lambda_trend", "nses_limit", "optimality_probability", "RunConfig", "RunRecord", "SampleSet", "derive_repetition_seed",
     "derive_walk_seed", "solve", "target_campaign", "throughput_report", "WalkConfig",
     "WalkResult", "WalkTrace", "key", "run_walk", "run_walk_traced", "MAX_EXHAUSTIVE_D",
     "exhaustive_optimum",
