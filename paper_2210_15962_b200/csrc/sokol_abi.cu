@@ -101,7 +101,10 @@ int validate(int L, int n, int64_t W) {
   return SK_OK;
 }
 
-constexpr int kWPB = 4;                  // warps per block (one walk per warp)
+#ifndef SK_WPB
+#define SK_WPB 4
+#endif
+constexpr int kWPB = SK_WPB;             // warps per block (one walk per warp)
 constexpr uint32_t kSmemKeysMax = 32768;  // keys in smem up to 32 KB per walk
 
 struct Plan {

@@ -32,7 +32,7 @@ def main():
     lengths = [int(x) for x in os.environ.get("SANITIZE_LENGTHS", "27,101,201,449").split(",")]
     for L in lengths:
         d = (L + 1) // 2
-        n = 8 * d
+        n = int(os.environ.get("SANITIZE_WF", "8")) * d  # walk factor (racecheck at L=449 needs short walks)
         layouts = [int(x) for x in os.environ.get("SANITIZE_LAYOUTS", "1,2,3").split(",")]
         for layout in layouts:
             for variant in (_lib.VARIANT_FAST, _lib.VARIANT_SCALAR):
