@@ -47,6 +47,11 @@
 #ifndef SK_TC_MIN_BLOCKS2
 #define SK_TC_MIN_BLOCKS2 3
 #endif
+// Independent HMMA accumulator chains per tile (2: alternate k-blocks and add
+// at the end; 1: one dependent chain, no FADD).
+#ifndef SK_TC_CHAINS
+#define SK_TC_CHAINS 2
+#endif
 
 namespace sk {
 
@@ -61,8 +66,6 @@ struct TcGeom {
   uint32_t go_off;    //                               odd-aligned copy at go_off + 2 (y + 9)
   uint32_t t_off;     // [TA_0 | TB_0 | TA_1 | TB_1]: TA_pi[i] at +2 (i + TOFF), TB_pi[i] at +2 (i + TOFF + 1)
   uint32_t s2_off;    // int8 S2[h] = 2 s_h (s_h at the centre h = K), h < D; 0 beyond
-  uint32_t r8_off;    // int8 parity-split spins for the R update: T8_pi[i] = s_{2i+pi} at r8_off + pi NT8 + T8OFF + i
-  int NT8, T8OFF;
   uint32_t bytes;
 };
 
@@ -89,11 +92,6 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
   o += 8u * uint32_t(g.NT);
   g.s2_off = o;
   o += 128u * uint32_t(g.MT) + 16u;
-  o = (o + 15u) & ~15u;
-  g.NT8 = (2 * g.K + 20 + 3) & ~3;  // reads h0 + pi - (x + pi) / 2 + {0, 2} in [-K, K + 8]
-  g.T8OFF = g.K + 8;
-  g.r8_off = o;
-  o += 2u * uint32_t(g.NT8);
   g.bytes = (o + 31u) & ~31u;
   return g;
 }
@@ -180,7 +178,7 @@ struct EvalTC {
   uint32_t b_pos, b_neg;    // B pair addresses at x0 = 2t - g (own-parity copy) / at -x0-1 (other copy)
   uint32_t b_m0;            // m = 0 pair: b_pos if x0 >= 0 else b_neg (then swapped)
   uint32_t sel_m0;          // byte_perm selector for it
-  uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile (s8, G or T8 addresses)
+  uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile (s8 or G addresses)
   int32_t Rk[MT][4];
   uint32_t inv[MT][4];
   uint32_t key[MT][4];
@@ -188,9 +186,8 @@ struct EvalTC {
   int32_t xq_e, xq_o;       // 512 qs for the even / odd neighbours of a lane (qs = (-1)^(D-1-h))
   int32_t m2xq_e, m2xq_o;   // -2 xq
   __half2 cq[CQ][2];        // C_{2j}, j = j0 .. j0+3, j0 = 128 r + 4 lane (lag-owned)
-  // move-role constants (lanes 0..12): address = fb + f4 (x>>2) + f2 ((x>>1)&1) + f1 (x&1)
-  uint32_t fb, f4, f2, f1;
-  int32_t r8_odd;           // NT8 + 1
+  // move-role constants (lanes 0..9): address = fb + f4 (x>>2) + 2 ((x>>1)&1) + f1 (x&1)
+  uint32_t fb, f4, f1;
   uint32_t t_base, ge_a, go_a, s8_a;  // shared addresses
 
   static uint32_t ext_bytes(int L, int) { return tc_geom(L).bytes; }
@@ -227,7 +224,6 @@ struct EvalTC {
     __half* ta = reinterpret_cast<__half*>(ext + G.t_off);
     __half* q = reinterpret_cast<__half*>(ext + G.q_off) + 8 * 32;
     int8_t* s2 = reinterpret_cast<int8_t*>(ext + G.s2_off);
-    int8_t* t8 = reinterpret_cast<int8_t*>(ext + G.r8_off);
     for (int h = lane; h < D; h += 32) s2[h] = int8_t(h == K ? s[h] : 2 * s[h]);
     for (int x = lane; x < P.L; x += 32) {
       const __half v = __int2half_rn(s[x]);
@@ -237,7 +233,6 @@ struct EvalTC {
       const int qo = 2 * pi + (i & 1);
       q[8 * (i >> 1) + qo] = v;
       q[8 * ((i >> 1) - 4) + 4 + qo] = v;
-      t8[pi * G.NT8 + G.T8OFF + i] = s[x];
     }
     t_base = ext_a + G.t_off;
     ge_a = ext_a + G.ge_off + 16u;  // address of G(0) in the even copy
@@ -265,7 +260,7 @@ struct EvalTC {
       cxb[tau] = cxcopy + uint32_t(2 * (K - h0a - 3));
       sxb[tau] = s8_a + uint32_t(3 * h0a - 2 * K);
       shb[tau] = s2_a + uint32_t(h0a);
-      r2b[tau] = ext_a + G.r8_off + uint32_t(G.T8OFF + h0a);  // R-update windows: T8 at h0 + (per-move offset)
+      r2b[tau] = s8_a + uint32_t(2 * h0a);
 #pragma unroll
       for (int f = 0; f < 4; f++) {
         const int h = h0[tau] + hoff(f);
@@ -291,23 +286,20 @@ struct EvalTC {
       cq[r][0] = __halves2half2(__int2half_rn(c[0]), __int2half_rn(c[1]));
       cq[r][1] = __halves2half2(__int2half_rn(c[2]), __int2half_rn(c[3]));
     }
-    // move roles (even lane: p, odd lane: q): 0,1 int8 sequence; 2,3 / 4,5
-    // even- / odd-aligned f16 spin copies; 6,7 / 8,9 the two Q records holding
-    // the spin; 10 the S2 cell of p; 11,12 the T8 cells of q, p
+    // move roles: 0,1 int8 sequence; 2,3 / 4,5 even- / odd-aligned f16 spin
+    // copies; 6,7 / 8,9 the two Q records holding the spin (even lane: p, odd: q)
+    // and lane 10 the S2 cell of p
     const int role = lane >> 1;
-    fb = s8_a, f4 = 4u, f2 = 2u, f1 = 1u;
-    if (role == 1 || role == 2) {
-      fb = t_base + 2u * G.TOFF + (role == 2 ? 2u * G.NT + 2u : 0u), f1 = 4u * G.NT;
-    } else if (role == 3 || role == 4) {
-      fb = ext_a + G.q_off + 512u - (role == 4 ? 56u : 0u), f4 = 16u, f1 = 4u;
-    } else if (lane == 10) {
-      fb = s2_a;
-    } else if (lane == 11 || lane == 12) {
-      fb = ext_a + G.r8_off + uint32_t(G.T8OFF), f4 = 2u, f2 = 1u, f1 = uint32_t(G.NT8);  // x>>1 + NT8 (x&1)
-    }
+    fb = role == 0 ? s8_a
+                   : role == 1 ? t_base + 2u * G.TOFF
+                   : role == 2 ? t_base + 2u * G.NT + 2u * G.TOFF + 2u
+                   : role == 3 ? ext_a + G.q_off + 512u
+                   : role == 4 ? ext_a + G.q_off + 512u - 56u
+                               : s2_a;
+    f4 = (role == 0 || role >= 5) ? 4u : role <= 2 ? 4u : 16u;
+    f1 = (role == 0 || role >= 5) ? 1u : role <= 2 ? 4u * G.NT : 4u;
     pin(qbase), pin(b_pos), pin(b_neg), pin(b_m0), pin(sel_m0), pin(xq_e), pin(xq_o), pin(m2xq_e), pin(m2xq_o);
-    r8_odd = G.NT8 + 1;
-    pin(fb), pin(f4), pin(f2), pin(f1), pin(t_base), pin(ge_a), pin(go_a), pin(s8_a), pin(r8_odd);
+    pin(fb), pin(f4), pin(f1), pin(t_base), pin(ge_a), pin(go_a), pin(s8_a);
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
       pin(cxb[tau]), pin(sxb[tau]), pin(shb[tau]), pin(r2b[tau]), pin(h0[tau]);
@@ -343,7 +335,7 @@ struct EvalTC {
       for (int tau = 0; tau < MT; tau++)
         if (m >= mlo(tau) && m <= mhi(tau)) {
           const uint4 a = lds128(qbase + 512u * tau + 128 * m);
-          mma_tc(acc[tau][(m - M_LO) & 1], a, b0, b1);
+          mma_tc(acc[tau][SK_TC_CHAINS == 2 ? ((m - M_LO) & 1) : 0], a, b0, b1);
         }
     }
     // key(h) = 64 dE + 2^29 + h = Rk + 512 qs C_{q-p} - s_h (xm 64 X + 2048 qs s_x)   (see header)
@@ -358,7 +350,7 @@ struct EvalTC {
 #pragma unroll
       for (int f = 0; f < 4; f++) {
         const int ho = hoff(f);
-        const int32_t X = __float2int_rz(acc[tau][0][f] + acc[tau][1][f]);
+        const int32_t X = __float2int_rz(SK_TC_CHAINS == 2 ? acc[tau][0][f] + acc[tau][1][f] : acc[tau][0][f]);
         const int32_t sx = lds8(sxb[tau] + 3 * ho);
         const int32_t sh = sext_byte(shq, ho);
         // S2 = 2 s_h: sh (-256 X - 2 xq s_x) = s_h (-512 X - 2048 qs s_x); at the
@@ -397,10 +389,10 @@ struct EvalTC {
     // this lane's scattered cell (lanes 0..9): position x of the move
     const int x = (lane & 1) ? q : p;
     const int32_t sxo = (lane & 1) ? sq : sp;
-    const uint32_t fa = fb + f4 * uint32_t(x >> 2) + f2 * uint32_t((x >> 1) & 1) + f1 * uint32_t(x & 1);
+    const uint32_t fa = fb + f4 * uint32_t(x >> 2) + 2u * uint32_t((x >> 1) & 1) + f1 * uint32_t(x & 1);
     __syncwarp();
     // the flipped spins read as 0 while C and R are updated
-    sts8_if(lane < 2 || lane == 11 || lane == 12, fa, 0);
+    sts8_if(lane < 2, fa, 0);
     sts16_if(lane >= 2 && lane < 6, fa, 0);
     __syncwarp();
     // C_{2j} += scale * v_j, v_j = s_{p-2j} + s_{p+2j} (apply_neighbor, _kernels.py:126-158)
@@ -438,13 +430,10 @@ struct EvalTC {
     {
       const int32_t wp = -4096 * sp, wq = centre ? 0 : -4096 * sq;
       const int pi = p & 1;
-      const int po = pi ? r8_odd : 0;  // NT8 + 1 selects T8_1 and the + pi
 #pragma unroll
       for (int tau = 0; tau < MT; tau++) {
-        // s_{2h-y} for h = h0 + pi + {0, 2}: T8_pi[h0 + pi - (y + pi) / 2 + {0, 2}] (conflict-free bytes)
-        const uint32_t bp = r2b[tau] + uint32_t(po - ((p + 1) >> 1));  // (y + pi) / 2 = (y + 1) >> 1
-        const uint32_t bq = r2b[tau] + uint32_t(po - ((q + 1) >> 1));
-        const int32_t vp0 = lds8(bp), vp1 = lds8(bp + 2), vq0 = lds8(bq), vq1 = lds8(bq + 2);
+        const uint32_t bp = r2b[tau] + uint32_t(2 * pi - p), bq = r2b[tau] + uint32_t(2 * pi - q);
+        const int32_t vp0 = lds8(bp), vp1 = lds8(bp + 4), vq0 = lds8(bq), vq1 = lds8(bq + 4);
         const int32_t d0 = wp * vp0 + wq * vq0, d1 = wp * vp1 + wq * vq1;
         if (pi == 0) {
           Rk[tau][0] += d0;
@@ -457,7 +446,7 @@ struct EvalTC {
     }
     __syncwarp();
     // the flipped spins: int8 sequence, f16 spin copies, Q records
-    sts8_if(lane < 2 || (lane >= 10 && lane < 13), fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
+    sts8_if(lane < 2 || lane == 10, fa, lane == 10 ? (centre ? -sp : -2 * sp) : -sxo);
     sts16_if(lane >= 2 && lane < 10, fa, sxo > 0 ? 0xBC00u : 0x3C00u);
     __syncwarp();
   }

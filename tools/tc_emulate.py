@@ -40,11 +40,6 @@ class Geom:
         o += 8 * self.NT
         self.s2_off = o
         o += 128 * self.MT + 16
-        o = (o + 15) & ~15
-        self.NT8 = (2 * self.K + 20 + 3) & ~3
-        self.T8OFF = self.K + 8
-        self.r8_off = o
-        o += 2 * self.NT8
         self.bytes = (o + 31) & ~31
         self.span_lo = (L + 8 + 3) & ~3
         self.span_hi = L + 16
@@ -93,7 +88,6 @@ class Emu:
             qo = 2 * pi + (i & 1)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * (i >> 1) + qo), v)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * ((i >> 1) - 4) + 4 + qo), v)
-            self.ext[self.t8addr(pi, i)] = int(s[x]) & 0xFF
         sigma = -1 if (D - 1) & 1 else 1
         self.xq = (512 * sigma, -512 * sigma)
         # per-lane registers
@@ -120,14 +114,6 @@ class Emu:
                 for u in range(4):
                     j = 128 * r + 4 * lane + u
                     self.cq[lane, r, u] = H(C[j] if 1 <= j <= K else 0)
-
-    def t8addr(self, pi, i):
-        g = self.g
-        return g.r8_off + pi * g.NT8 + g.T8OFF + i
-
-    def t8v(self, pi, i):
-        b = self.ext[self.t8addr(pi, i)]
-        return b - 256 if b > 127 else b
 
     # byte-level access ------------------------------------------------------
     def st16(self, off, v):
@@ -224,7 +210,6 @@ class Emu:
         # zero pass
         for x in {p, q}:
             self.s8[g.span_lo + x] = 0
-            self.ext[self.t8addr(x & 1, x >> 1)] = 0
             pi, i = x & 1, x >> 1
             self.st16(g.t_off + 2 * (2 * pi * g.NT + g.TOFF + i), H(0))
             self.st16(g.t_off + 2 * ((2 * pi + 1) * g.NT + g.TOFF + 1 + i), H(0))
@@ -255,16 +240,15 @@ class Emu:
             for tau in range(g.MT):
                 h0 = 128 * tau + 16 * gg + 4 * t
                 h0a = h0 if h0 <= K else (K & ~3)
-                ip, iq = h0a + pi - ((p + pi) >> 1), h0a + pi - ((q + pi) >> 1)
-                vp0, vp1 = self.t8v(pi, ip), self.t8v(pi, ip + 2)
-                vq0, vq1 = self.t8v(pi, iq), self.t8v(pi, iq + 2)
+                base = 2 * h0a + 2 * pi
+                vp0, vp1 = self.s8v(base - p), self.s8v(base + 4 - p)
+                vq0, vq1 = self.s8v(base - q), self.s8v(base + 4 - q)
                 f0 = 0 if pi == 0 else 2
                 self.Rk[lane, tau, f0] += wp * vp0 + wq * vq0
                 self.Rk[lane, tau, f0 + 1] += wp * vp1 + wq * vq1
         # final pass
         for x, sxo in ((p, sp), (q, sq)):
             self.s8[g.span_lo + x] = (-sxo) & 0xFF
-            self.ext[self.t8addr(x & 1, x >> 1)] = (-sxo) & 0xFF
             v = H(-sxo)
             pi2, i = x & 1, x >> 1
             self.st16(g.t_off + 2 * (2 * pi2 * g.NT + g.TOFF + i), v)
