@@ -47,6 +47,9 @@
 #ifndef SK_TC_MIN_BLOCKS2
 #define SK_TC_MIN_BLOCKS2 3
 #endif
+#ifndef SK_TC_MIN_BLOCKS4
+#define SK_TC_MIN_BLOCKS4 2
+#endif
 // Independent HMMA accumulator chains per tile (2: alternate k-blocks and add
 // at the end; 1: one dependent chain, no FADD).
 #ifndef SK_TC_CHAINS
@@ -55,7 +58,10 @@
 
 namespace sk {
 
-constexpr int kTcMaxL = 511;  // D <= 256: at most two 128-neighbour tiles
+#ifndef SK_TC_MAX_L
+#define SK_TC_MAX_L 511
+#endif
+constexpr int kTcMaxL = SK_TC_MAX_L;  // 511: D <= 256, at most two 128-neighbour tiles
 
 // Byte offsets inside the evaluator's shared-memory area (host and device).
 struct TcGeom {
@@ -199,9 +205,9 @@ struct EvalTC {
   __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}
   static bool supports(int L) { return L >= 3 && L <= kTcMaxL; }
   static constexpr bool kNeedsDl = false;
-  static constexpr bool kSmemKeysVariant = true;
+  static constexpr bool kSmemKeysVariant = MT <= 2;  // per-layout kernels only where they pay (L <= 511)
   static constexpr bool kCeAliasKeys = true;
-  static constexpr int kMinBlocks = MT == 1 ? SK_TC_MIN_BLOCKS1 : SK_TC_MIN_BLOCKS2;
+  static constexpr int kMinBlocks = MT == 1 ? SK_TC_MIN_BLOCKS1 : (MT == 2 ? SK_TC_MIN_BLOCKS2 : SK_TC_MIN_BLOCKS4);
   // s8 reads: R update 2h - x in [-(L-1), 2K + 12], s_{3h-2K} in [-2K, K + 18],
   // position 0 kept 4-byte aligned (the s_h quad is one LDS.32)
   static int span_lo(int L, int) { return (L + 8 + 3) & ~3; }

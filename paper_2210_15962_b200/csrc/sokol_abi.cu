@@ -250,6 +250,24 @@ int dispatch_tc(int L, F&& f) {
     case 15: return dispatch_tc_at<15>(f);
     case 16: return dispatch_tc_at<16>(f);
 #endif
+#if SK_TC_MAX_L > 511
+    case 17: return dispatch_tc_at<17>(f);
+    case 18: return dispatch_tc_at<18>(f);
+    case 19: return dispatch_tc_at<19>(f);
+    case 20: return dispatch_tc_at<20>(f);
+    case 21: return dispatch_tc_at<21>(f);
+    case 22: return dispatch_tc_at<22>(f);
+    case 23: return dispatch_tc_at<23>(f);
+    case 24: return dispatch_tc_at<24>(f);
+    case 25: return dispatch_tc_at<25>(f);
+    case 26: return dispatch_tc_at<26>(f);
+    case 27: return dispatch_tc_at<27>(f);
+    case 28: return dispatch_tc_at<28>(f);
+    case 29: return dispatch_tc_at<29>(f);
+    case 30: return dispatch_tc_at<30>(f);
+    case 31: return dispatch_tc_at<31>(f);
+    case 32: return dispatch_tc_at<32>(f);
+#endif
   }
   return fail(SK_ERR_UNSUPPORTED, "no EvalTC instantiation for this length");
 }
