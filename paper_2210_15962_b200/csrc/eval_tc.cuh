@@ -1,4 +1,4 @@
-// eval_tc.cuh -- production neighbourhood evaluator for L <= 511 (SK_VARIANT_FAST).
+// eval_tc.cuh -- production neighbourhood evaluator (SK_VARIANT_FAST), every L <= SK_MAX_L.
 //
 // Same exact arithmetic as the reference's neighbor_delta / apply_neighbor
 // (_kernels.py:85-158), restated for one warp per walk:
@@ -59,9 +59,9 @@
 namespace sk {
 
 #ifndef SK_TC_MAX_L
-#define SK_TC_MAX_L 511
+#define SK_TC_MAX_L 1023
 #endif
-constexpr int kTcMaxL = SK_TC_MAX_L;  // 511: D <= 256, at most two 128-neighbour tiles
+constexpr int kTcMaxL = SK_TC_MAX_L;  // = SK_MAX_L: D <= 512, up to four 128-neighbour tiles
 
 // Byte offsets inside the evaluator's shared-memory area (host and device).
 struct TcGeom {

@@ -206,6 +206,7 @@ int launch_nw(Plan& pl, cudaStream_t st, int dev) {
 // MT = ceil(NW/2) and, for one tile, a compile-time MMA count).  Every
 // launch -- walks, traces, the evaluator probe -- goes through here, so the
 // probe runs exactly the instantiation the batch kernel runs.
+#ifdef SK_OLD_FAST_EVALUATOR
 template <int NW, class F>
 int dispatch_fast_small(int L, F&& f) {
   const sk::FastGeom g = sk::fast_geom(L);
@@ -221,6 +222,7 @@ int dispatch_fast_small(int L, F&& f) {
   }
   return f(NWc{}, (sk::EvalFast<1, 0>*)nullptr);
 }
+#endif
 
 // L <= 511: the one- / two-tile evaluator with a compile-time k-block count
 // (NI = ceil(D / 16) fixes the word count too: nw = ceil(NI / 4)).
@@ -250,7 +252,7 @@ int dispatch_tc(int L, F&& f) {
     case 15: return dispatch_tc_at<15>(f);
     case 16: return dispatch_tc_at<16>(f);
 #endif
-#if SK_TC_MAX_L > 511
+#if SK_TC_MAX_L > 511 && !defined(SK_TC_ONE_TILE_ONLY)
     case 17: return dispatch_tc_at<17>(f);
     case 18: return dispatch_tc_at<18>(f);
     case 19: return dispatch_tc_at<19>(f);
@@ -288,12 +290,13 @@ int dispatch_eval(int L, int nw, bool scalar, F&& f) {
     return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
   }
 #ifndef SK_OLD_FAST_EVALUATOR
+  // production: the transposed-signal evaluator for every supported length
 #ifdef SK_TC_ONE_TILE_ONLY
-  if (L <= 255) return dispatch_tc(L, f);
+  if (L > 255) return fail(SK_ERR_UNSUPPORTED, "one-tile development build");
+#endif
+  return dispatch_tc(L, f);
 #else
-  if (L <= sk::kTcMaxL) return dispatch_tc(L, f);
-#endif
-#endif
+  // round-1 evaluator, kept for A/B reference builds (-DSK_OLD_FAST_EVALUATOR)
   switch (nw) {
     case 1: return dispatch_fast_small<1>(L, f);
     case 2: return dispatch_fast_small<2>(L, f);
@@ -305,6 +308,7 @@ int dispatch_eval(int L, int nw, bool scalar, F&& f) {
     case 8: return f(std::integral_constant<int, 8>{}, (sk::EvalFast<4>*)nullptr);
   }
   return fail(SK_ERR_UNSUPPORTED, "unsupported word count");
+#endif
 }
 
 template <bool TRACE>
@@ -334,8 +338,8 @@ int run(int L, int n, const uint64_t* seeds, uint64_t master, uint64_t batch, ui
   std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
   SK_CUDA(cudaGetDevice(&dev));
-  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
-  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalTC<1>::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalTC<1>>(L, n);
   pl.P.seeds = seeds;
   pl.P.master = master;
   pl.P.batch = batch;
@@ -555,8 +559,8 @@ int64_t sk_resident_walks(int L, int n) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   std::lock_guard<std::mutex> lk(g_mu);
-  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
-  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalFast<1>>(L, n);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalTC<1>::supports(L);
+  Plan pl = scalar ? make_plan<sk::EvalScalar>(L, n) : make_plan<sk::EvalTC<1>>(L, n);
   pl.P.W = int64_t(1) << 40;
   pl.dry_run = true;
   const int rc = launch_walks<false>(pl, scalar, 0, dev);
@@ -651,7 +655,7 @@ int sk_eval_states(int L, int64_t S, const int8_t* d_halves, int M, const int32_
   SK_CUDA(cudaGetDevice(&dev));
   SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int D = (L + 1) / 2, nw = (D + 63) / 64;
-  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalFast<1>::supports(L);
+  const bool scalar = g_variant == SK_VARIANT_SCALAR || !sk::EvalTC<1>::supports(L);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return dispatch_eval(L, nw, scalar, [&](auto nwc, auto* evp) {
     using Eval = std::remove_pointer_t<decltype(evp)>;

@@ -22,7 +22,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 import tc_emulate  # noqa: E402
 
 
-@pytest.mark.parametrize("L", [3, 5, 7, 27, 63, 101, 129, 201, 253, 255, 257, 301, 449, 511])
+@pytest.mark.parametrize("L", [3, 5, 7, 27, 63, 101, 129, 201, 253, 255, 257, 301, 449, 511, 513, 769, 1023])
 def test_emulated_evaluator_matches_oracle(oracle, L):
     d = (L + 1) // 2
     rng = np.random.default_rng(L)
