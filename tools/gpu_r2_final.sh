@@ -21,3 +21,9 @@ for tool in memcheck synccheck racecheck; do
     > gpurun_out/${T}_sanitize_$tool.log 2>&1; echo "$tool rc=$?"; tail -2 gpurun_out/${T}_sanitize_$tool.log
 done
 fi
+if [ "${SANITIZE_LONG:-0}" = "1" ]; then
+for tool in memcheck racecheck; do
+  SANITIZE_LENGTHS=513,1023 SANITIZE_LAYOUTS=2,3 SANITIZE_W=2 SANITIZE_WF=1 timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py \
+    > gpurun_out/${T}_sanitize_long_$tool.log 2>&1; echo "$tool (L=513,1023) rc=$?"; tail -2 gpurun_out/${T}_sanitize_long_$tool.log
+done
+fi
