@@ -48,7 +48,6 @@ out = {
     "registers": get("launch__registers_per_thread"),
     "inst_executed": get("smsp__inst_executed.sum"),
     "smem_wavefronts": get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
-    "smem_wavefronts_ideal": get("smsp__sass_inst_executed_op_shared.sum") and get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
     "smem_wavefronts_pct": get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
     "smem_ld_bank_conflict_share": (get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum") or 0)
     / max(1.0, get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum") or 1.0),
