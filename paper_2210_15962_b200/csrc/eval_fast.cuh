@@ -154,6 +154,7 @@ struct EvalFast {
   static uint32_t block_bytes(int) { return 0; }  // no per-block table
   __device__ static void block_init(const WalkParams&, char*, int, int) {}
   __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}  // nothing to prefetch
+  __device__ __forceinline__ void renormalize(const WalkParams&, int) {}     // no drifting state
 
   __device__ __forceinline__ void init(const WalkParams& P, WarpSmem& sm, int8_t* s, int lane) {
     G = fast_geom(P.L);

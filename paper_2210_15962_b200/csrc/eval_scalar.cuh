@@ -42,6 +42,7 @@ struct EvalScalar {
   static uint32_t block_bytes(int) { return 0; }  // no per-block table
   __device__ static void block_init(const WalkParams&, char*, int, int) {}
   __device__ __forceinline__ void prefetch(const WalkParams&, int, int) {}  // nothing to prefetch
+  __device__ __forceinline__ void renormalize(const WalkParams&, int) {}     // no drifting state
 
   __device__ __forceinline__ void init(const WalkParams&, WarpSmem&, int8_t*, int) {}
 

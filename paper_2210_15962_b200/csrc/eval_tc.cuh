@@ -42,10 +42,10 @@
 // Blocks per SM (4 warps each) the one- / two-tile kernels are register-capped
 // for; overridable at build time for experiments.
 #ifndef SK_TC_MIN_BLOCKS1
-#define SK_TC_MIN_BLOCKS1 4
+#define SK_TC_MIN_BLOCKS1 5
 #endif
 #ifndef SK_TC_MIN_BLOCKS2
-#define SK_TC_MIN_BLOCKS2 3
+#define SK_TC_MIN_BLOCKS2 4
 #endif
 #ifndef SK_TC_MIN_BLOCKS4
 #define SK_TC_MIN_BLOCKS4 2
@@ -61,6 +61,11 @@ namespace sk {
 #ifndef SK_TC_MAX_L
 #define SK_TC_MAX_L 1023
 #endif
+// Rk of a padding slot (h >= D).  Its S2 and C_{q-p} read zero cells, so its
+// key is its Rk, which the R update moves by at most 8192 per step: from
+// 3 * 2^30 it stays in [2^30, 2^32) for kRenormSteps = 2^16 steps, i.e. above
+// every real key (< kKeyLimit = 2^30), and renormalize() resets it.
+constexpr int32_t kVirtualRk = int32_t(0xC0000000u);
 constexpr int kTcMaxL = SK_TC_MAX_L;  // = SK_MAX_L: D <= 512, up to four 128-neighbour tiles
 
 // Byte offsets inside the evaluator's shared-memory area (host and device).
@@ -186,7 +191,6 @@ struct EvalTC {
   uint32_t sel_m0;          // byte_perm selector for it
   uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile (s8 or G addresses)
   int32_t Rk[MT][4];
-  uint32_t inv[MT][4];
   uint32_t key[MT][4];
   int32_t h0[MT];
   int32_t xq_e, xq_o;       // 512 qs for the even / odd neighbours of a lane (qs = (-1)^(D-1-h))
@@ -262,10 +266,13 @@ struct EvalTC {
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
       h0[tau] = 128 * tau + 16 * g + 4 * t;
-      const int h0a = h0[tau] <= K ? h0[tau] : (K & ~3);  // padding lanes read in-range cells
-      cxb[tau] = cxcopy + uint32_t(2 * (K - h0a - 3));
+      // padding lanes (h0 > K) read in-range cells, with S2 and C_{q-p} from
+      // zero cells so that their keys are exactly their Rk (see kVirtualRk)
+      const bool padl = h0[tau] > K;
+      const int h0a = padl ? (K & ~3) : h0[tau];
+      cxb[tau] = cxcopy + uint32_t(2 * (padl ? -8 + ((K + 1) & 1) : K - h0a - 3));
       sxb[tau] = s8_a + uint32_t(3 * h0a - 2 * K);
-      shb[tau] = s2_a + uint32_t(h0a);
+      shb[tau] = s2_a + uint32_t(padl ? 128 * MT : h0a);
       r2b[tau] = s8_a + uint32_t(2 * h0a);
 #pragma unroll
       for (int f = 0; f < 4; f++) {
@@ -277,8 +284,8 @@ struct EvalTC {
           for (int j = 1; 2 * j <= h; j++) r += int32_t(s[h - 2 * j]) * int32_t(s[h + 2 * j]);
         const int32_t c0 = 16 * (centre ? (h >> 1) : (K - 1 - pi));
         // the centre's s_x term is the constant S2[K] m2xq s_K = -2 xq (s_x = s_K): cancelled here
-        Rk[tau][f] = 64 * c0 + 2048 * r + (1 << 29) + h + (centre ? 2 * (f < 2 ? xq_e : xq_o) : 0);
-        inv[tau][f] = live ? 0u : ~0u;
+        Rk[tau][f] = live ? 64 * c0 + 2048 * r + (1 << 29) + h + (centre ? 2 * (f < 2 ? xq_e : xq_o) : 0)
+                          : kVirtualRk;
       }
     }
 #pragma unroll
@@ -309,8 +316,6 @@ struct EvalTC {
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
       pin(cxb[tau]), pin(sxb[tau]), pin(shb[tau]), pin(r2b[tau]), pin(h0[tau]);
-#pragma unroll
-      for (int f = 0; f < 4; f++) pin(inv[tau][f]);
     }
     __syncwarp();
   }
@@ -362,10 +367,18 @@ struct EvalTC {
         // S2 = 2 s_h: sh (-256 X - 2 xq s_x) = s_h (-512 X - 2048 qs s_x); at the
         // centre S2 = s_K gives -256 s_K X and the constant cancelled in Rk
         const int32_t k = Rk[tau][f] + (f < 2 ? xq_e : xq_o) * cx[f] + sh * (-256 * X + (f < 2 ? m2xq_e : m2xq_o) * sx);
-        if (trace_row && !inv[tau][f]) trace_row[h0[tau] + ho] = (k - (1 << 29) - (h0[tau] + ho)) >> 6;
-        key[tau][f] = uint32_t(k) | inv[tau][f];
+        if (trace_row && h0[tau] + ho < P.D) trace_row[h0[tau] + ho] = (k - (1 << 29) - (h0[tau] + ho)) >> 6;
+        key[tau][f] = uint32_t(k);  // padding slots: exactly their Rk, >= kKeyLimit
       }
     }
+  }
+
+  __device__ __forceinline__ void renormalize(const WalkParams& P, int) {
+#pragma unroll
+    for (int tau = 0; tau < MT; tau++)
+#pragma unroll
+      for (int f = 0; f < 4; f++)
+        if (h0[tau] + hoff(f) >= P.D) Rk[tau][f] = kVirtualRk;
   }
 
   __device__ __forceinline__ uint32_t local_min() const {

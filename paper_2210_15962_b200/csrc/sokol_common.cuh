@@ -28,6 +28,9 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kHBits = 9;
 constexpr int32_t kBias = 1 << 20;
 constexpr uint32_t kNoCand = 0xffffffffu;
+// Every real candidate key ((delta/8 + kBias) << kHBits | h) is below 2^30;
+// a warp minimum at or above it means no unvisited neighbour is left.
+constexpr uint32_t kKeyLimit = 1u << 30;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // _kernels.py:32-37
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -98,6 +98,7 @@ struct SmemLayout {
 };
 
 constexpr int32_t kExcluded = 0x7fffffff;
+constexpr int kRenormSteps = 1 << 16;
 
 // KS = 1: the visited keys are in shared memory (compile-time; see VisitedSet)
 template <int NW, bool TRACE, class Eval, int KS>
@@ -188,7 +189,12 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   int steps = 0;
   bool dead = false;
   int last = -1;  // half index of the previous move: N_last = P_{t-1} is visited
-  for (int step = 0; step < n; step++) {
+  // Steps run in chunks of kRenormSteps; between chunks the evaluator may
+  // re-normalise state that drifts by a bounded amount per step (EvalTC's
+  // padding slots), at no per-step cost.
+  for (int base = 0; base < n && !dead; base += kRenormSteps) {
+  const int lim = n - base < kRenormSteps ? n : base + kRenormSteps;
+  for (int step = base; step < lim; step++) {
     // ---- neighbourhood (_kernels.py:239-243) ----------------------------
     ev.evaluate(P, sm, s, lane, TRACE ? P.trace_deltas + (int64_t(w) * n + step) * D : nullptr);
     // undoing the last move returns to P_{t-1}, whose key is in the set:
@@ -201,7 +207,7 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
     uint64_t fbit = 0;
     for (;;) {
       const uint32_t m = warp_min_u32(ev.local_min());
-      if (m == kNoCand) break;
+      if (m >= kKeyLimit) break;
       const int hc = cand_h(m);
       ev.prefetch(P, hc, lane);  // the move's operands load while the candidate is probed
       uint64_t chain[NW];
@@ -238,6 +244,8 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
       for (int i = 0; i < NW; i++) best_w[i] = words[i];
     }
   }
+  ev.renormalize(P, lane);
+  }
 
   // ---- outputs (_kernels.py:283-287) and batch reduction ------------------
   if (lane == 0) {
@@ -259,8 +267,17 @@ __device__ __forceinline__ void run_one_walk(const WalkParams& P, const SmemLayo
   __syncwarp();
 }
 
+// Register cap for kMinBlocks resident blocks: 64K registers per SM, allocated
+// per warp in units of 8 per thread.  Set with __maxnreg__ (a hard cap) rather
+// than __launch_bounds__' minimum-blocks hint, which makes ptxas aim well
+// below the cap.
+template <class Eval, int WPB>
+constexpr int kMaxRegs = (65536 / (Eval::kMinBlocks * WPB * 32)) / 8 * 8 > 255
+                             ? 255
+                             : (65536 / (Eval::kMinBlocks * WPB * 32)) / 8 * 8;
+
 template <int NW, bool TRACE, class Eval, int WPB, int KS = 0>
-__global__ void __launch_bounds__(WPB * 32, Eval::kMinBlocks) saw_walk_kernel(WalkParams P, SmemLayout lay) {
+__global__ void __launch_bounds__(WPB * 32) __maxnreg__((kMaxRegs<Eval, WPB>)) saw_walk_kernel(WalkParams P, SmemLayout lay) {
   extern __shared__ __align__(128) char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;

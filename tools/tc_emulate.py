@@ -58,6 +58,8 @@ def mhi(NI, tau):
 
 
 HOFF = (0, 2, 1, 3)
+VIRTUAL_RK = 0xC0000000 - (1 << 32)  # int32 of 3 * 2^30: padding slots' Rk
+KEY_LIMIT = 1 << 30
 
 
 class Emu:
@@ -105,8 +107,8 @@ class Emu:
                         r = sum(int(s[h - 2 * j]) * int(s[h + 2 * j]) for j in range(1, h // 2 + 1)
                                 if h + 2 * j < L)
                     c0 = 16 * ((h >> 1) if centre else (K - 1 - (h & 1)))
-                    self.Rk[lane, tau, f] = (64 * c0 + 2048 * r + (1 << 29) + h
-                                             + (2 * self.xq[f >= 2] if centre else 0))
+                    self.Rk[lane, tau, f] = ((64 * c0 + 2048 * r + (1 << 29) + h
+                                              + (2 * self.xq[f >= 2] if centre else 0)) if live else VIRTUAL_RK)
                     self.inv[lane, tau, f] = not live
         self.cq = {}
         for lane in range(32):
@@ -181,10 +183,11 @@ class Emu:
             for lane in range(32):
                 gg, t = lane >> 2, lane & 3
                 h0 = 128 * tau + 16 * gg + 4 * t
-                h0a = h0 if h0 <= g.K else (g.K & ~3)
+                padl = h0 > g.K
+                h0a = (g.K & ~3) if padl else h0
                 frag = [(gg, 2 * t), (gg, 2 * t + 1), (gg + 8, 2 * t), (gg + 8, 2 * t + 1)]
-                y0 = g.K - h0a - 3
                 copy = 1 if (g.K + 1) & 1 else 0
+                y0 = (-8 + ((g.K + 1) & 1)) if padl else g.K - h0a - 3  # padding lanes: zero cells
                 p1 = self.gpair(y0, copy)
                 p2 = self.gpair(y0 + 2, copy)
                 cx = [int(p2[1]), int(p1[1]), int(p2[0]), int(p1[0])]
@@ -193,11 +196,14 @@ class Emu:
                     X = int(Y[0, r, c] + Y[1, r, c])
                     ho = HOFF[f]
                     sx = self.s8v(3 * (h0a + ho) - 2 * g.K)
-                    sh = self.s2v(h0a + ho)
+                    sh = self.s2v(128 * g.MT) if padl else self.s2v(h0a + ho)
                     xq = self.xq[f >= 2]
                     k = self.Rk[lane, tau, f] + xq * cx[f] + sh * (-256 * X + (-2 * xq) * sx)
                     if not self.inv[lane, tau, f]:
                         out[h0 + ho] = (k - (1 << 29) - (h0 + ho)) >> 6
+                        assert 0 < k < KEY_LIMIT
+                    else:  # a padding slot's key is exactly its Rk, never a candidate
+                        assert k == self.Rk[lane, tau, f] and (k & 0xFFFFFFFF) >= KEY_LIMIT
                     keys[lane, tau, f] = k
         return out
 
