@@ -32,15 +32,19 @@
 // HADD2 + two HFMA2 on half2 registers from parity-split f16 spin arrays
 // (two shifted copies, so every spin pair is one aligned LDS.32), then
 // stored to both G copies.  R_h (sum_j s_{h-2j} s_{h+2j}) changes in O(1)
-// per neighbour.  Then 10 scattered cells (int8 sequence, f16 spin copies,
-// Q records) take the flipped spins: two stores.
+// per neighbour.  Then 11 scattered cells (int8 sequence, f16 spin copies,
+// Q records, S2) take the flipped spins: two predicated stores.
+//
+// Padding slots (h >= D) have no mask: their operands read zero cells, so
+// their key is their Rk (kVirtualRk, kept above every real key; see below).
 #pragma once
 #include <cuda_fp16.h>
 
 #include "walk_engine.cuh"
 
-// Blocks per SM (4 warps each) the one- / two-tile kernels are register-capped
-// for; overridable at build time for experiments.
+// Blocks per SM (4 warps each) the one- / two- / three-or-four-tile kernels
+// are register-capped for (__maxnreg__, walk_engine.cuh); measured
+// (DESIGN.md §4), overridable at build time for experiments.
 #ifndef SK_TC_MIN_BLOCKS1
 #define SK_TC_MIN_BLOCKS1 5
 #endif
