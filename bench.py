@@ -5,7 +5,8 @@
 One "step" = one batch of walks (BASELINE config 4): every GPU runs
 `--walkers-per-gpu` (default 2^20) independent walks of n = 8*D steps at
 L=201 with seeds derived on device from (master_seed=1, batch, global walker),
-then the batch is merged across ranks (NCCL all-reduce MIN/SUM, 16-88 B).
+then the batch is merged across ranks (one NCCL all_gather of the per-rank
+summaries, ~32 B per rank).
 Weak scaling: per-GPU work is fixed as N grows.
 
 value  = sum over ranks of steps*(D-1) / max over ranks of the device time of
@@ -239,7 +240,7 @@ def run_native(args):
         flush.zero_()
         starts[b].record(stream)
         launch(b)
-        res = merge()  # 80-byte D2H (+ NCCL MIN/SUM across ranks)
+        res = merge()  # 80-byte D2H (+ one NCCL all_gather across ranks)
         ends[b].record(stream)
         total_steps += res.steps_sum
         if best is None or res.best_E < best:
@@ -350,22 +351,16 @@ def host_seeds(master, batch, begin, W):
 
 def mma_per_step(L: int) -> int:
     """mma.sync.m16n8k16 per walk step of the production evaluator
-    (eval_tc.cuh for L <= 511: sum over 128-neighbour tiles of the k-block
-    range [mlo(tau), mhi(tau)]; eval_fast.cuh above: the padded block count
-    per 8-column tile)."""
+    (eval_tc.cuh, every L <= 1023): the sum over 128-neighbour tiles tau of
+    the k-block range [mlo(tau), mhi(tau)]."""
     D = (L + 1) // 2
-    if L <= 511:
-        NI = (D + 15) // 16
-        MT = (NI + 7) // 8
-        tot = 0
-        for tau in range(MT):
-            amax = min(8 * tau + 7, NI - 1)
-            tot += (NI - 4 * tau - 1) - (-((amax + 1) >> 1)) + 1
-        return tot
-    NB = ((D - 1) >> 1) // 16 + 1
     NI = (D + 15) // 16
-    NT = (2 * NB + 7) // 8
-    return NT * (((NI - 1 + NB - 1 + 1) + 1) & ~1)
+    MT = (NI + 7) // 8
+    tot = 0
+    for tau in range(MT):
+        amax = min(8 * tau + 7, NI - 1)
+        tot += (NI - 4 * tau - 1) - (-((amax + 1) >> 1)) + 1
+    return tot
 
 
 def roofline(L, n, W, nse_per_s_gpu, dev_ms, clocks):
