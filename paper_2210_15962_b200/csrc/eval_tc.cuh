@@ -25,14 +25,16 @@
 //     h0 = 128 tau + 16 g + 4 t, so the epilogue's per-neighbour operands
 //     (C_{q-p}, s_x, s_h) come from a few vector loads.
 //
-// A move (apply_neighbor, _kernels.py:126-158): every lane owns four
-// consecutive lags per 128 (j0 = 128 r + 4 l): C_{2j} -= 4 s_p v_j(h*) with
+// A move (apply_neighbor, _kernels.py:126-158): every lane owns two
+// consecutive lags per 64 (j0 = 64 r + 2 l): C_{2j} -= 4 s_p v_j(h*) with
 // v_j = s_{p-2j} + s_{p+2j} (the flipped positions p, q read as zero, which
-// removes the excluded lag q - p and the own lag j = 0), computed as two
-// HADD2 + two HFMA2 on half2 registers from parity-split f16 spin arrays
+// removes the excluded lag q - p and the own lag j = 0), computed as one
+// HADD2 + one HFMA2 on a half2 register from parity-split f16 spin arrays
 // (two shifted copies, so every spin pair is one aligned LDS.32), then
-// stored to both G copies.  R_h (sum_j s_{h-2j} s_{h+2j}) changes in O(1)
-// per neighbour.  Then 11 scattered cells (int8 sequence, f16 spin copies,
+// stored to both G copies.  Consecutive lanes touch consecutive 4-byte words,
+// so none of these accesses has a bank conflict (a quad per lane, 8-byte
+// lane stride, costs two wavefronts per 4-byte access).
+// R_h (sum_j s_{h-2j} s_{h+2j}) changes in O(1) per neighbour.  Then 11 scattered cells (int8 sequence, f16 spin copies,
 // Q records, S2) take the flipped spins: two predicated stores.
 //
 // Padding slots (h >= D) have no mask: their operands read zero cells, so
@@ -75,10 +77,13 @@ constexpr int kTcMaxL = SK_TC_MAX_L;  // = SK_MAX_L: D <= 512, up to four 128-ne
 // Byte offsets inside the evaluator's shared-memory area (host and device).
 struct TcGeom {
   int D, K, NI, MT;
-  int NT, TOFF;       // f16 spin arrays: NT halves each, index i at TOFF + i (+1 in the odd-aligned copy)
+  int NT, TOFF;       // f16 spin arrays: NT halves each, index i at TOFF + i (+1 in the odd-aligned copy);
+                      // cells outside the sequence are zero
   uint32_t q_off;     // Q records: record r in [-32, 8 NI + 24) at q_off + 16 (r + 32)
   uint32_t ge_off;    // G(y), y in [-8, 128 MT + 8): even-aligned copy at ge_off + 2 (y + 8)
   uint32_t go_off;    //                               odd-aligned copy at go_off + 2 (y + 9)
+                      // (each 4 bytes past a 16-byte boundary where that makes the epilogue's
+                      // C_{q-p} quad, G(K - 3 - h0 .. K - h0), 8-byte aligned)
   uint32_t t_off;     // [TA_0 | TB_0 | TA_1 | TB_1]: TA_pi[i] at +2 (i + TOFF), TB_pi[i] at +2 (i + TOFF + 1)
   uint32_t s2_off;    // int8 S2[h] = 2 s_h (s_h at the centre h = K), h < D; 0 beyond
   uint32_t bytes;
@@ -93,16 +98,19 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
   uint32_t o = 0;
   g.q_off = o;
   o += 16u * uint32_t(8 * g.NI + 56);
-  g.ge_off = o;
-  o += 2u * uint32_t(128 * g.MT + 16);
+  g.ge_off = o + (((g.K - 3) & 3) == 2 ? 4u : 0u);
+  o += 2u * uint32_t(128 * g.MT + 16) + 16u;
   o = (o + 15u) & ~15u;
-  g.go_off = o;
-  o += 2u * uint32_t(128 * g.MT + 20);
+  g.go_off = o + (((g.K - 3) & 3) == 1 ? 4u : 0u);
+  o += 2u * uint32_t(128 * g.MT + 20) + 16u;
   o = (o + 15u) & ~15u;
-  g.NT = 3 * g.K + 20;
-  g.NT += g.NT & 1;
-  g.TOFF = g.K + 8;
+  // the move's lag pairs j < 64 NG (NG = ceil(NI / 4)) read T_pi at P1 +- j
+  // without clamping: past K they read zero cells, so v_j = 0 there
+  const int ng = (g.NI + 3) / 4;
+  g.TOFF = g.K + 8 > 64 * ng + 2 ? g.K + 8 : 64 * ng + 2;
   g.TOFF += g.TOFF & 1;
+  g.NT = 3 * g.K + 20 > g.TOFF + g.K / 2 + 64 * ng + 4 ? 3 * g.K + 20 : g.TOFF + g.K / 2 + 64 * ng + 4;
+  g.NT += g.NT & 1;
   g.t_off = o;
   o += 8u * uint32_t(g.NT);
   g.s2_off = o;
@@ -117,6 +125,11 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld64s(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t ld32s(uint32_t a) {
@@ -139,13 +152,14 @@ __device__ __forceinline__ void sts16_if(bool c, uint32_t a, uint32_t v) {
                "r"(int(c))
                : "memory");
 }
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(uint16_t(v)) : "memory");
+}
 __device__ __forceinline__ void sts32_if(bool c, uint32_t a, uint32_t v) {
   asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p st.shared.b32 [%0], %1; }" ::"r"(a), "r"(v), "r"(int(c))
-               : "memory");
-}
-__device__ __forceinline__ void sts64_if(bool c, uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("{ .reg .pred p; setp.ne.b32 p, %3, 0; @p st.shared.v2.b32 [%0], {%1, %2}; }" ::"r"(a), "r"(x), "r"(y),
-               "r"(int(c))
                : "memory");
 }
 // v if a != b else ~0 (a SEL; a plain ternary on an unrolled constant b can
@@ -179,7 +193,7 @@ __device__ __forceinline__ __half2 u2h(uint32_t v) { return *reinterpret_cast<__
 template <int NI>
 struct EvalTC {
   static constexpr int MT = (NI + 7) / 8;  // 128-neighbour tiles
-  static constexpr int CQ = MT;            // lag quads per lane (K < 128 MT)
+  static constexpr int NG = (NI + 3) / 4;  // lag pairs per lane (K < 64 NG)
   static constexpr int M_LO = -(NI >> 1);  // k-blocks of the product
   static constexpr int M_HI = NI - 1;
   __host__ __device__ static constexpr int amax(int tau) { return (8 * tau + 7 < NI - 1) ? 8 * tau + 7 : NI - 1; }
@@ -193,16 +207,17 @@ struct EvalTC {
   uint32_t b_pos, b_neg;    // B pair addresses at x0 = 2t - g (own-parity copy) / at -x0-1 (other copy)
   uint32_t b_m0;            // m = 0 pair: b_pos if x0 >= 0 else b_neg (then swapped)
   uint32_t sel_m0;          // byte_perm selector for it
-  uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile (s8 or G addresses)
+  uint32_t cxb[MT], sxb[MT], shb[MT], r2b[MT];  // epilogue / R-update bases per tile
   int32_t Rk[MT][4];
   uint32_t key[MT][4];
   int32_t h0[MT];
   int32_t xq_e, xq_o;       // 512 qs for the even / odd neighbours of a lane (qs = (-1)^(D-1-h))
   int32_t m2xq_e, m2xq_o;   // -2 xq
-  __half2 cq[CQ][2];        // C_{2j}, j = j0 .. j0+3, j0 = 128 r + 4 lane (lag-owned)
-  // move-role constants (lanes 0..9): address = fb + f4 (x>>2) + 2 ((x>>1)&1) + f1 (x&1)
+  __half2 cq[NG];           // C_{2j}, j = j0, j0 + 1, j0 = 64 r + 2 lane (lag-owned)
+  // move-role constants (lanes 0..10): address = fb + f4 (x>>2) + 2 ((x>>1)&1) + f1 (x&1)
   uint32_t fb, f4, f1;
-  uint32_t t_base, ge_a, go_a, s8_a;  // shared addresses
+  uint32_t t_base, s8_a;    // shared addresses
+  uint32_t ge_l, go_l;      // G(2 lane) in the even / odd copy
 
   static uint32_t ext_bytes(int L, int) { return tc_geom(L).bytes; }
   // No per-block table and no prefetch: both were measured (a table of the
@@ -249,8 +264,10 @@ struct EvalTC {
       q[8 * ((i >> 1) - 4) + 4 + qo] = v;
     }
     t_base = ext_a + G.t_off;
-    ge_a = ext_a + G.ge_off + 16u;  // address of G(0) in the even copy
-    go_a = ext_a + G.go_off + 18u;  // ... in the odd copy
+    const uint32_t ge_a = ext_a + G.ge_off + 16u;  // address of G(0) in the even copy
+    const uint32_t go_a = ext_a + G.go_off + 18u;  // ... in the odd copy
+    ge_l = ge_a + 4u * uint32_t(lane);
+    go_l = go_a + 4u * uint32_t(lane);
     s8_a = uint32_t(__cvta_generic_to_shared(s));
     const int g = lane >> 2, t = lane & 3;
     qbase = ext_a + G.q_off + 16u * uint32_t(32 + 4 * g + t);
@@ -274,9 +291,9 @@ struct EvalTC {
       // zero cells so that their keys are exactly their Rk (see kVirtualRk)
       const bool padl = h0[tau] > K;
       const int h0a = padl ? (K & ~3) : h0[tau];
-      cxb[tau] = cxcopy + uint32_t(2 * (padl ? -8 + ((K + 1) & 1) : K - h0a - 3));
+      cxb[tau] = cxcopy + uint32_t(2 * (padl ? -8 + ((K - 3) & 3) : K - h0a - 3));  // 8-byte aligned
       sxb[tau] = s8_a + uint32_t(3 * h0a - 2 * K);
-      shb[tau] = s2_a + uint32_t(padl ? 128 * MT : h0a);
+      shb[tau] = s2_a + uint32_t(h0[tau]);  // zero cells beyond D, in the same 128-byte row
       r2b[tau] = s8_a + uint32_t(2 * h0a);
 #pragma unroll
       for (int f = 0; f < 4; f++) {
@@ -293,15 +310,10 @@ struct EvalTC {
       }
     }
 #pragma unroll
-    for (int r = 0; r < CQ; r++) {
-      int32_t c[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int j = 128 * r + 4 * lane + u;
-        c[u] = (j >= 1 && j <= K) ? sm.ce[j] : 0;
-      }
-      cq[r][0] = __halves2half2(__int2half_rn(c[0]), __int2half_rn(c[1]));
-      cq[r][1] = __halves2half2(__int2half_rn(c[2]), __int2half_rn(c[3]));
+    for (int r = 0; r < NG; r++) {
+      const int j = 64 * r + 2 * lane;
+      const int c0 = (j >= 1 && j <= K) ? sm.ce[j] : 0, c1 = (j + 1 <= K) ? sm.ce[j + 1] : 0;
+      cq[r] = __halves2half2(__int2half_rn(c0), __int2half_rn(c1));
     }
     // move roles: 0,1 int8 sequence; 2,3 / 4,5 even- / odd-aligned f16 spin
     // copies; 6,7 / 8,9 the two Q records holding the spin (even lane: p, odd: q)
@@ -316,7 +328,7 @@ struct EvalTC {
     f4 = (role == 0 || role >= 5) ? 4u : role <= 2 ? 4u : 16u;
     f1 = (role == 0 || role >= 5) ? 1u : role <= 2 ? 4u * G.NT : 4u;
     pin(qbase), pin(b_pos), pin(b_neg), pin(b_m0), pin(sel_m0), pin(xq_e), pin(xq_o), pin(m2xq_e), pin(m2xq_o);
-    pin(fb), pin(f4), pin(f1), pin(t_base), pin(ge_a), pin(go_a), pin(s8_a);
+    pin(fb), pin(f4), pin(f1), pin(t_base), pin(ge_l), pin(go_l), pin(s8_a);
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
       pin(cxb[tau]), pin(sxb[tau]), pin(shb[tau]), pin(r2b[tau]), pin(h0[tau]);
@@ -356,8 +368,9 @@ struct EvalTC {
     // key(h) = 64 dE + 2^29 + h = Rk + 512 qs C_{q-p} - s_h (xm 64 X + 2048 qs s_x)   (see header)
 #pragma unroll
     for (int tau = 0; tau < MT; tau++) {
-      const uint32_t cp1 = ld32s(cxb[tau]);       // (C_{q-p} of h0+3, of h0+2)
-      const uint32_t cp2 = ld32s(cxb[tau] + 4);   // (h0+1, h0)
+      const uint2 cpq = ld64s(cxb[tau]);
+      const uint32_t cp1 = cpq.x;                 // (C_{q-p} of h0+3, of h0+2)
+      const uint32_t cp2 = cpq.y;                 // (h0+1, h0)
       const uint32_t shq = ld32s(shb[tau]);       // S2[h0 .. h0+3]
       const __half2 c12 = u2h(cp1), c34 = u2h(cp2);
       const int32_t cx[4] = {__half2int_rz(__high2half(c34)), __half2int_rz(__high2half(c12)),
@@ -424,27 +437,19 @@ struct EvalTC {
       const __half2 scale = __half2half2(__int2half_rn(centre ? -2 * sp : -4 * sp));
       const TcGeom G = tc_geom(P.L);
       const uint32_t ua = t_base + 2u * uint32_t(G.NT * (2 * pi + par) + P1 + G.TOFF + par);
-      const uint32_t ub = t_base + 2u * uint32_t(G.NT * (2 * pi + 1 - par) + P1 - 3 + G.TOFF + 1 - par);
+      const uint32_t ub = t_base + 2u * uint32_t(G.NT * (2 * pi + 1 - par) + P1 - 1 + G.TOFF + 1 - par);
+      const uint32_t al = ua + 4u * uint32_t(lane), bl = ub - 4u * uint32_t(lane);
 #pragma unroll
-      for (int r = 0; r < CQ; r++) {
-        // lanes past K read a valid quad (clamped) and store nothing: no branch
-        const int j0 = 128 * r + 4 * lane;
-        const bool act = j0 <= K;
-        const int jr = act ? j0 : 0;
-        {
-          const uint32_t aa = ua + 2u * uint32_t(jr), ab = ub - 2u * uint32_t(jr);
-          const __half2 A0 = u2h(ld32s(aa)), A1 = u2h(ld32s(aa + 4));
-          const __half2 B0 = u2h(ld32s(ab)), B1 = u2h(ld32s(ab + 4));
-          const __half2 v01 = __hadd2(A0, __lowhigh2highlow(B1));
-          const __half2 v23 = __hadd2(A1, __lowhigh2highlow(B0));
-          cq[r][0] = __hfma2(v01, scale, cq[r][0]);
-          cq[r][1] = __hfma2(v23, scale, cq[r][1]);
-          const uint32_t c0 = h2u(cq[r][0]), c1v = h2u(cq[r][1]);
-          sts64_if(act, ge_a + 2u * uint32_t(jr), c0, c1v);
-          sts16_if(act, go_a + 2u * uint32_t(jr), c0);
-          sts32_if(act, go_a + 2u * uint32_t(jr) + 2u, __byte_perm(c0, c1v, 0x5432));
-          sts16_if(act, go_a + 2u * uint32_t(jr) + 6u, c1v >> 16);
-        }
+      for (int r = 0; r < NG; r++) {
+        // lag pair (j, j + 1), j = 64 r + 2 lane: 32 lanes x 4 consecutive bytes
+        // per access, no bank conflict.  Past K, v_j reads zero cells, so those
+        // C stay 0 and the unpredicated stores write the zeros the cells hold.
+        const __half2 A = u2h(ld32s(al + 128u * r)), B = u2h(ld32s(bl - 128u * r));
+        cq[r] = __hfma2(__hadd2(A, __lowhigh2highlow(B)), scale, cq[r]);
+        const uint32_t c = h2u(cq[r]);
+        sts32(ge_l + 128u * r, c);
+        sts16(go_l + 128u * r, c);
+        sts16(go_l + 128u * r + 2u, c >> 16);
       }
     }
     // R_h: the terms s_y s_{2h-y}, y in {p, q}, change sign (same-parity

@@ -26,16 +26,18 @@ class Geom:
         o = 0
         self.q_off = o
         o += 16 * (8 * self.NI + 56)
-        self.ge_off = o
-        o += 2 * (128 * self.MT + 16)
+        self.ge_off = o + (4 if ((self.K - 3) & 3) == 2 else 0)
+        o += 2 * (128 * self.MT + 16) + 16
         o = (o + 15) & ~15
-        self.go_off = o
-        o += 2 * (128 * self.MT + 20)
+        self.go_off = o + (4 if ((self.K - 3) & 3) == 1 else 0)
+        o += 2 * (128 * self.MT + 20) + 16
         o = (o + 15) & ~15
-        self.NT = 3 * self.K + 20
-        self.NT += self.NT & 1
-        self.TOFF = self.K + 8
+        self.NG = (self.NI + 3) // 4
+        ng = (self.NI + 3) // 4
+        self.TOFF = max(self.K + 8, 64 * ng + 2)
         self.TOFF += self.TOFF & 1
+        self.NT = max(3 * self.K + 20, self.TOFF + self.K // 2 + 64 * ng + 4)
+        self.NT += self.NT & 1
         self.t_off = o
         o += 8 * self.NT
         self.s2_off = o
@@ -112,9 +114,9 @@ class Emu:
                     self.inv[lane, tau, f] = not live
         self.cq = {}
         for lane in range(32):
-            for r in range(g.MT):
-                for u in range(4):
-                    j = 128 * r + 4 * lane + u
+            for r in range(g.NG):
+                for u in range(2):
+                    j = 64 * r + 2 * lane + u
                     self.cq[lane, r, u] = H(C[j] if 1 <= j <= K else 0)
 
     # byte-level access ------------------------------------------------------
@@ -187,7 +189,8 @@ class Emu:
                 h0a = (g.K & ~3) if padl else h0
                 frag = [(gg, 2 * t), (gg, 2 * t + 1), (gg + 8, 2 * t), (gg + 8, 2 * t + 1)]
                 copy = 1 if (g.K + 1) & 1 else 0
-                y0 = (-8 + ((g.K + 1) & 1)) if padl else g.K - h0a - 3  # padding lanes: zero cells
+                y0 = (-8 + ((g.K - 3) & 3)) if padl else g.K - h0a - 3  # padding lanes: zero cells
+                assert ((g.go_off + 18 if copy else g.ge_off + 16) + 2 * y0) % 8 == 0  # one LDS.64
                 p1 = self.gpair(y0, copy)
                 p2 = self.gpair(y0 + 2, copy)
                 cx = [int(p2[1]), int(p1[1]), int(p2[0]), int(p1[0])]
@@ -196,7 +199,7 @@ class Emu:
                     X = int(Y[0, r, c] + Y[1, r, c])
                     ho = HOFF[f]
                     sx = self.s8v(3 * (h0a + ho) - 2 * g.K)
-                    sh = self.s2v(128 * g.MT) if padl else self.s2v(h0a + ho)
+                    sh = self.s2v(h0 + ho)  # padding lanes: zero cells h >= D
                     xq = self.xq[f >= 2]
                     k = self.Rk[lane, tau, f] + xq * cx[f] + sh * (-256 * X + (-2 * xq) * sx)
                     if not self.inv[lane, tau, f]:
@@ -222,22 +225,23 @@ class Emu:
         P1, pi, par = p >> 1, p & 1, (p >> 1) & 1
         scale = H(-2 * sp if centre else -4 * sp)
         ua = g.t_off + 2 * (g.NT * (2 * pi + par) + P1 + g.TOFF + par)
-        ub = g.t_off + 2 * (g.NT * (2 * pi + 1 - par) + P1 - 3 + g.TOFF + 1 - par)
+        ub = g.t_off + 2 * (g.NT * (2 * pi + 1 - par) + P1 - 1 + g.TOFF + 1 - par)
         for lane in range(32):
-            for r in range(g.MT):
-                j0 = 128 * r + 4 * lane
-                if j0 > K:
-                    continue
+            for r in range(g.NG):
+                j0 = 64 * r + 2 * lane  # every lane, unpredicated: past K the pair stays 0
                 aa, ab = ua + 2 * j0, ub - 2 * j0
                 assert aa % 4 == 0 and ab % 4 == 0
-                A0 = (self.ld16(aa), self.ld16(aa + 2))
-                A1 = (self.ld16(aa + 4), self.ld16(aa + 6))
-                B0 = (self.ld16(ab), self.ld16(ab + 2))
-                B1 = (self.ld16(ab + 4), self.ld16(ab + 6))
-                v = [A0[0] + B1[1], A0[1] + B1[0], A1[0] + B0[1], A1[1] + B0[0]]
-                for u in range(4):
+                for a in (aa, ab):  # inside the row
+                    row = (a - g.t_off) // (2 * g.NT)
+                    assert 0 <= row < 4 and (a + 2 - g.t_off) // (2 * g.NT) == row
+                A = (self.ld16(aa), self.ld16(aa + 2))
+                B = (self.ld16(ab), self.ld16(ab + 2))
+                v = [A[0] + B[1], A[1] + B[0]]
+                for u in range(2):
                     self.cq[lane, r, u] = H(float(v[u]) * float(scale) + float(self.cq[lane, r, u]))
-                for u in range(4):
+                    assert j0 + u <= K or float(self.cq[lane, r, u]) == 0.0
+                assert (g.ge_off + 16 + 2 * j0) % 4 == 0 and (g.go_off + 18 + 2 * j0) % 4 == 2
+                for u in range(2):
                     self.st16(g.ge_off + 16 + 2 * (j0 + u), self.cq[lane, r, u])
                     self.st16(g.go_off + 18 + 2 * (j0 + u), self.cq[lane, r, u])
         wp, wq = -4096 * sp, (0 if centre else -4096 * sq)
