@@ -111,6 +111,10 @@ __host__ __device__ inline TcGeom tc_geom(int L) {
   g.TOFF += g.TOFF & 1;
   g.NT = 3 * g.K + 20 > g.TOFF + g.K / 2 + 64 * ng + 4 ? 3 * g.K + 20 : g.TOFF + g.K / 2 + 64 * ng + 4;
   g.NT += g.NT & 1;
+  // rows 2 NT bytes apart must not land on the same bank: the move's flip
+  // stores write TA_pi[i] and TB_pi[i] (adjacent rows) in one instruction
+  if ((g.NT & 63) < 8) g.NT += 8 - (g.NT & 63);
+  else if ((g.NT & 63) > 56) g.NT += 72 - (g.NT & 63);
   g.t_off = o;
   o += 8u * uint32_t(g.NT);
   g.s2_off = o;

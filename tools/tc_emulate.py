@@ -38,6 +38,11 @@ class Geom:
         self.TOFF += self.TOFF & 1
         self.NT = max(3 * self.K + 20, self.TOFF + self.K // 2 + 64 * ng + 4)
         self.NT += self.NT & 1
+        if self.NT % 64 < 8:  # adjacent spin rows on different banks
+            self.NT += 8 - self.NT % 64
+        elif self.NT % 64 > 56:
+            self.NT += 72 - self.NT % 64
+        assert 16 <= (2 * self.NT) % 128 <= 112
         self.t_off = o
         o += 8 * self.NT
         self.s2_off = o
