@@ -272,3 +272,46 @@ class Emu:
             self.st16(g.q_off + 2 * (8 * 32 + 8 * (i >> 1) + qo), v)
             self.st16(g.q_off + 2 * (8 * 32 + 8 * ((i >> 1) - 4) + 4 + qo), v)
         self.ext[g.s2_off + p] = (-sp if centre else -2 * sp) & 0xFF
+
+
+def check_geometry(L):
+    """The layout properties EvalTC relies on, for every lane, tile, lag pair and
+    move at length L (vectorised; the emulator above exercises them on data):
+    disjoint regions, the epilogue's C_{q-p} quad one aligned 8-byte load, the
+    move's unclamped spin reads inside their row and past K on zero cells, the
+    C stores inside the G copies, adjacent spin rows on different banks."""
+    g = Geom(L)
+    K, NG, MT, NT, TOFF = g.K, g.NG, g.MT, g.NT, g.TOFF
+    regions = [(g.q_off, 16 * (8 * g.NI + 56)), (g.ge_off, 2 * (128 * MT + 16)), (g.go_off, 2 * (128 * MT + 20)),
+               (g.t_off, 8 * NT), (g.s2_off, 128 * MT + 16)]
+    for (a, n), (b, _) in zip(regions, regions[1:]):
+        assert a + n <= b, (L, a, n, b)
+    assert regions[-1][0] + regions[-1][1] <= g.bytes
+    assert 16 <= (2 * NT) % 128 <= 112, (L, NT)  # adjacent spin rows start on different banks
+    # epilogue: G(K - 3 - h0 .. K - h0) (zero cells y0 in [-8, -5] for padding lanes), one aligned LDS.64
+    h0 = (128 * np.arange(MT)[:, None] + 16 * (np.arange(32) >> 2) + 4 * (np.arange(32) & 3)).ravel()
+    y0 = np.where(h0 > K, -8 + ((K - 3) & 3), K - h0 - 3)
+    base = g.go_off + 18 if (K + 1) & 1 else g.ge_off + 16
+    assert np.all((base + 2 * y0) % 8 == 0), L
+    # the move: lag pair j = 64 r + 2 lane, every lane, unpredicated
+    p = np.arange(K + 1)[:, None, None]
+    lane = np.arange(32)[None, :, None]
+    r = np.arange(NG)[None, None, :]
+    j = 64 * r + 2 * lane
+    P1, pi = p >> 1, p & 1
+    par = P1 & 1
+    ia = P1 + TOFF + par + j  # row 2 pi + par: (T[ia], T[ia + 1])
+    ib = P1 - 1 + TOFF + 1 - par - j  # row 2 pi + 1 - par: (T[ib], T[ib + 1])
+    for idx, row_par in ((ia, par), (ib, 1 - par)):
+        assert idx.min() >= 0 and idx.max() + 1 < NT, (L, idx.min(), idx.max(), NT)
+        # position held by row (pi, shift) at index I: x = 2 (I - TOFF - shift) + pi
+        for off in (0, 1):
+            x = 2 * (idx + off - TOFF - row_par) + pi
+            far = (j + off > K) if idx is ia else (j + 1 - off > K)
+            inside = (x >= 0) & (x < L)
+            assert not np.any(far & inside), L
+    # the C stores: G(j), G(j + 1) in both copies, inside their regions
+    jmax = 64 * NG - 1
+    assert g.ge_off + 16 + 2 * jmax + 2 <= g.ge_off + 2 * (128 * MT + 16)
+    assert g.go_off + 18 + 2 * jmax + 2 <= g.go_off + 2 * (128 * MT + 20)
+    return g
